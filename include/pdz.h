@@ -1,0 +1,223 @@
+/*
+ * pdz.h -- C ABI of the B200 (sm_100a) dehazing library  libpdz.so
+ *
+ * Drop-in boundary for the hot path of pdehaze 0.1.0 (arXiv 2506.08793).
+ * The reference has no FFI: its boundary is the Python API of
+ * pdehaze.solver / pdehaze.scattering (re-exported by pdehaze/__init__.py:10-36).
+ * Each entry point below replaces one of those functions; the Python package
+ * paper_2506_08793_b200 binds them with ctypes and keeps
+ * the reference names, signatures and exceptions.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers unless the parameter name ends in
+ *     `_host`.  Buffers are caller-owned; the library keeps no pointer after a
+ *     call returns and allocates no device memory: scratch comes from a caller
+ *     workspace whose size the matching *_workspace_bytes() reports.
+ *   - Images are interleaved [H][W][C] (the reference's (H, W, C) C-order
+ *     layout, image.py:3-6), float64 or float32 (`image_is_f64`).
+ *   - Solver fields are planar float32: plane p of P = batch*C planes at
+ *     offset p*H*W, rows of W samples.  The transmission-driven weight
+ *     lambda has one plane per image (shared by its C channels).
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t) and returns a
+ *     status code; pdz_last_error() holds a thread-local message.
+ *       PDZ_OK         success
+ *       PDZ_EINVAL     bad shape / range / configuration  -> ValueError
+ *       PDZ_ENONFINITE solver produced non-finite values  -> FloatingPointError
+ *       PDZ_ECUDA      CUDA runtime failure               -> RuntimeError
+ *       PDZ_EWORKSPACE workspace too small                -> ValueError
+ */
+#ifndef PDZ_H_
+#define PDZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDZ_OK 0
+#define PDZ_EINVAL 1
+#define PDZ_ENONFINITE 2
+#define PDZ_ECUDA 3
+#define PDZ_EWORKSPACE 4
+
+/* lambda_mode values (solver.py:262, :414-417) */
+#define PDZ_LAMBDA_AS_PRINTED 0 /* lambda0 * exp(-beta * (1 - t))      */
+#define PDZ_LAMBDA_PROSE 1      /* lambda0 * exp(-beta * t)            */
+#define PDZ_LAMBDA_ZERO 2       /* ablation "no-nonlocal": lambda == 0 */
+#define PDZ_LAMBDA_CONST 3      /* ablation "no-adaptive": == lambda0  */
+
+/* Geometry + numerics of one relaxed fixed-point solve over P planes.
+ * Mirrors the solver fields of SolverConfig (solver.py:78-89). */
+typedef struct pdz_solve_params {
+  int32_t height;          /* H >= 2 (divergence_term, solver.py:200-201)   */
+  int32_t width;           /* W >= 2                                        */
+  int32_t planes;          /* P = batch * channels                          */
+  int32_t channels;        /* C: planes p share lambda plane p / C          */
+  int32_t kernel_size;     /* odd >= 1, Gaussian support (solver.py:80)     */
+  int32_t edge_preserving; /* 0: D == 1 (ablation "no-edge", solver.py:420) */
+  int32_t max_iters;       /* >= 1                                          */
+  int32_t reserved;
+  double sigma;            /* Gaussian width (solver.py:79)                 */
+  double epsilon;          /* diffusion stabiliser (solver.py:78)           */
+  double tau;              /* relaxation step, 0 allowed for one step       */
+  double rel_tol;          /* relative residual-change stop (solver.py:88)  */
+} pdz_solve_params;
+
+/* ---- library ----------------------------------------------------------- */
+int32_t pdz_version(void);
+const char* pdz_last_error(void);
+
+/* Normalised 1-D Gaussian factor g/sum(g), g = exp(-d^2/2 sigma^2): the 2-D
+ * kernel of gaussian_kernel (solver.py:213-222) is outer(w, w).  Host call. */
+int32_t pdz_gaussian_taps(double sigma, int32_t kernel_size, double* taps_host);
+
+/* ---- DCP front end (scattering.py:48-139) ------------------------------ */
+/* Scratch needed by pdz_dark_channel / pdz_multiscale_dark_channel. */
+size_t pdz_dark_channel_workspace_bytes(int32_t height, int32_t width);
+
+/* dark_channel (scattering.py:48-65): min over channels of I_c / A_c (float64
+ * divide, :60), border-truncated (2r+1)^2 window minimum (van Herk/Gil-Werman,
+ * :61-64), capped at 1 (:65).  `airlight` is a device float64[C]. */
+int32_t pdz_dark_channel(const void* image, int32_t image_is_f64, int32_t height,
+                         int32_t width, int32_t channels, const double* airlight,
+                         int32_t radius, double* dark, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* multiscale_dark_channel (scattering.py:68-85): w0*d0 + w1*d1 + ... in
+ * radius order, float64 multiply-then-add (no FMA contraction). */
+int32_t pdz_multiscale_dark_channel(const void* image, int32_t image_is_f64, int32_t height,
+                                    int32_t width, int32_t channels, const double* airlight,
+                                    const int32_t* radii_host, const double* weights_host,
+                                    int32_t n_radii, double* dark, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/* Number of pixels estimate_atmospheric_light averages: ceil(fraction*H*W)
+ * in float64 (scattering.py:102). */
+int64_t pdz_airlight_count(int32_t height, int32_t width, double fraction);
+size_t pdz_airlight_workspace_bytes(int32_t height, int32_t width, double fraction);
+
+/* estimate_atmospheric_light (scattering.py:88-107): radix-select the count
+ * largest dark values, order them by (value desc, flat index asc) exactly like
+ * the stable argsort at :105, average I over them with a sequential float64
+ * sum in that order (:106-107), clip to [0.05, 1].  Writes airlight (device
+ * float64[C]) and, if non-NULL, the ordered flat indices (device int64[count]). */
+int32_t pdz_atmospheric_light(const void* image, int32_t image_is_f64, int32_t height,
+                              int32_t width, int32_t channels, const double* dark,
+                              double fraction, double* airlight, int64_t* picked,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* estimate_transmission (scattering.py:110-121): t = 1 - omega * dark. */
+int32_t pdz_transmission(const double* dark, int32_t height, int32_t width, double omega,
+                         double* transmission, void* stream);
+
+/* Solver inputs for one image: Phi_c = (I_c - A_c (1 - t)) / max(t, t0)
+ * (solver.py:324, scattering.py:138-139) as planar float32 [C][H][W], and
+ * lambda(t) (solver.py:244-263 or the ablation overrides :414-417) as float32
+ * [H][W].  Also returns the float64 Phi if phi64 != NULL (for "no-pde"). */
+int32_t pdz_solver_fields(const void* image, int32_t image_is_f64, int32_t height,
+                          int32_t width, int32_t channels, const double* transmission,
+                          const double* airlight, double t_floor, int32_t lambda_mode,
+                          double lambda0, double beta, float* phi, float* lambda_map,
+                          double* phi64, void* stream);
+
+/* adaptive_lambda (solver.py:244-263) in float64 over n samples of t;
+ * mode is PDZ_LAMBDA_AS_PRINTED or PDZ_LAMBDA_PROSE. */
+int32_t pdz_adaptive_lambda(const double* transmission, int64_t n, int32_t mode,
+                            double lambda0, double beta, double* out, void* stream);
+
+/* ---- guided-filter refinement (refine.py:21-80), SURVEY 8(f) next #1 ---- */
+size_t pdz_guided_workspace_bytes(int32_t height, int32_t width);
+/* box_mean (refine.py:21-40): border-truncated (2r+1)^2 mean from an integral
+ * image built with the reference's sequential cumsum order (bit-exact). */
+int32_t pdz_box_mean(const double* field, int32_t height, int32_t width, int32_t radius,
+                     double* out, void* workspace, size_t workspace_bytes, void* stream);
+/* guided_filter (refine.py:43-62). */
+int32_t pdz_guided_filter(const double* guide, const double* target, int32_t height,
+                          int32_t width, int32_t radius, double reg, double* out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+/* refine_transmission (refine.py:65-80): luminance guide, clip to [0, 1]. */
+int32_t pdz_refine_transmission(const void* image, int32_t image_is_f64, int32_t height,
+                                int32_t width, int32_t channels, const double* t_raw,
+                                int32_t radius, double reg, double* t_out, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* ---- PDE operators (solver.py:152-302) --------------------------------- */
+/* diffusion_coefficient (solver.py:152-164): 1 / (g + eps) over n samples. */
+int32_t pdz_diffusion_coefficient(const double* grad_magnitude, int64_t n, double epsilon,
+                                  double* out, void* stream);
+
+/* tau_stability_bound (solver.py:266-277) per plane at u: 2/(8 max D + max(max
+ * lambda, 0)), D edge-preserving.  bound: device float64[P]. */
+size_t pdz_tau_bound_workspace_bytes(const pdz_solve_params* params);
+int32_t pdz_tau_bound(const pdz_solve_params* params, const float* u, const float* lambda_map,
+                      double* bound, void* workspace, size_t workspace_bytes, void* stream);
+int32_t pdz_tau_bound_f64(const pdz_solve_params* params, const double* u,
+                          const double* lambda_map, double* bound, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* Operator probes for the API functions divergence_term (solver.py:190-210)
+ * and gaussian_convolve (:225-241) on P planes (float32 in/out). */
+int32_t pdz_divergence(const pdz_solve_params* params, const float* u, float* div,
+                       void* stream);
+int32_t pdz_divergence_f64(const pdz_solve_params* params, const double* u, double* div,
+                           void* stream);
+size_t pdz_gaussian_workspace_bytes(const pdz_solve_params* params, int32_t is_f64);
+int32_t pdz_gaussian(const pdz_solve_params* params, const float* u, float* out,
+                     void* workspace, size_t workspace_bytes, void* stream);
+int32_t pdz_gaussian_f64(const pdz_solve_params* params, const double* u, double* out,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- relaxed fixed-point sweep (the hot kernel) ------------------------- */
+size_t pdz_step_workspace_bytes(const pdz_solve_params* params);
+
+/* fixed_point_step (solver.py:280-302) on all P planes at once: one fused
+ * sweep u_out = u + tau * r, r = div(D grad u) - lambda G(u) + Phi, with
+ * ||r||_2 per plane (device float64[P]) and a per-plane non-finite flag
+ * (device int32[P]). */
+int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, float* u_out,
+                             const float* phi, const float* lambda_map, double* norms,
+                             int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+size_t pdz_solve_workspace_bytes(const pdz_solve_params* params);
+
+/* fixed_point_solve (solver.py:305-359) for all P planes: u0 = Phi, sweeps
+ * until each plane's relative residual change <= rel_tol (never at iteration
+ * 1) or max_iters.  Planes stop independently, like the reference's
+ * per-channel loop.  u_out (device float32 [P][H][W]) receives each plane's
+ * final iterate (after its stopping update, unclamped).  Host outputs:
+ * norms_host [max_iters][P] (row it-1 = iteration it), iterations_host[P],
+ * converged_host[P], failed_host[P] (0, or the iteration whose values went
+ * non-finite).  Returns PDZ_ENONFINITE if any plane failed.  Synchronises
+ * `stream` before returning. */
+int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
+                              const float* lambda_map, float* u_out, double* norms_host,
+                              int32_t* iterations_host, int32_t* converged_host,
+                              int32_t* failed_host, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* Asynchronous fixed-iteration variant for benchmarking: exactly
+ * params->max_iters sweeps (rel_tol ignored) captured in a CUDA graph,
+ * norms left on the device in the workspace.  Returns immediately. */
+int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float* phi,
+                                     const float* lambda_map, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+/* Number of kernels pdz_fixed_point_sweeps_async launches for `params`
+ * (benchmark bookkeeping). */
+int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);
+/* Device pointer to the plane-p final iterate inside a solve workspace after
+ * pdz_fixed_point_sweeps_async (buffer parity of `iterations`). */
+const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* workspace,
+                                    int32_t plane, int32_t iterations);
+
+/* clamp01 + interleave (solver.py:434, image.py:56-61): planar float32 P=C
+ * planes -> [H][W][C] float32 or float64 in [0, 1]. */
+int32_t pdz_clamp_interleave(const float* planes, int32_t height, int32_t width,
+                             int32_t channels, void* out, int32_t out_is_f64, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDZ_H_ */

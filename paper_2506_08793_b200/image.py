@@ -1,0 +1,93 @@
+"""Array conventions at the API boundary (pdehaze/image.py:34-61).
+
+Host (numpy) inputs are validated here exactly like the reference (float64
+coercion, layout, finiteness); device (torch.cuda) inputs are validated with
+device reductions and stay on the GPU.  `to_device` / `to_host` move data
+between the two worlds; the compute itself is always the CUDA library.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["validate_image", "validate_field", "clamp01", "is_device_array", "to_device",
+           "to_host"]
+
+
+def is_device_array(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _finite(x) -> bool:
+    if is_device_array(x):
+        import torch
+
+        return bool(torch.isfinite(x).all().item())
+    return bool(np.all(np.isfinite(x)))
+
+
+def validate_image(image):
+    """(H, W, C) with C in {1, 3}, H, W >= 1, all finite."""
+    arr = image if is_device_array(image) else np.asarray(image, dtype=np.float64)
+    shape = tuple(arr.shape)
+    if len(shape) != 3 or shape[2] not in (1, 3):
+        raise ValueError(f"expected (H, W, C) image with C in {{1, 3}}, got shape {shape}")
+    if shape[0] < 1 or shape[1] < 1:
+        raise ValueError(f"image dimensions must be >= 1, got shape {shape}")
+    if not _finite(arr):
+        raise ValueError("image contains non-finite values")
+    return arr
+
+
+def validate_field(field):
+    """(H, W) with all samples finite."""
+    arr = field if is_device_array(field) else np.asarray(field, dtype=np.float64)
+    if len(arr.shape) != 2:
+        raise ValueError(f"expected (H, W) scalar field, got shape {tuple(arr.shape)}")
+    if not _finite(arr):
+        raise ValueError("field contains non-finite values")
+    return arr
+
+
+def clamp01(values):
+    """Clip to [0, 1]; rejects non-finite input (image.py:56-61)."""
+    if is_device_array(values):
+        if not _finite(values):
+            raise ValueError("cannot clamp non-finite values")
+        return values.clamp(0.0, 1.0)
+    arr = np.asarray(values, dtype=np.float64)
+    if not np.all(np.isfinite(arr)):
+        raise ValueError("cannot clamp non-finite values")
+    return np.clip(arr, 0.0, 1.0)
+
+
+def to_device(x, dtype=None):
+    """numpy / torch -> contiguous CUDA tensor (float64 unless dtype given or
+    the tensor is already float32/float64 on the device)."""
+    import torch
+
+    from ._native import device
+
+    dev = device()
+    if is_device_array(x):
+        t = x
+        if dtype is not None and t.dtype != dtype:
+            t = t.to(dtype)
+        elif t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        return t.to(dev, non_blocking=True).contiguous()
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64 if dtype is None else
+                                          {torch.float32: np.float32,
+                                           torch.float64: np.float64}[dtype]))
+    return torch.from_numpy(arr).to(dev)
+
+
+def to_host(t, like) -> object:
+    """Return `t` as the caller's kind: numpy float64 for host callers."""
+    if is_device_array(like):
+        return t
+    return t.detach().to("cpu").numpy().astype(np.float64, copy=False)

@@ -1,0 +1,497 @@
+"""Relaxed fixed-point dehazing solve on B200 (drop-in for pdehaze.solver).
+
+Public functions keep the reference names, signatures, defaults and error
+behaviour (pdehaze/solver.py:152-446).  The work runs in libpdz.so:
+
+* `fixed_point_step` / `fixed_point_solve` / `dehaze` -> the fused float32
+  sweep kernel (csrc/pdz_sweep.cu), all channels (and, for `dehaze_batch`,
+  all images) of a solve in one launch per iteration, iterations replayed
+  from a captured CUDA graph, stop rule evaluated on the device;
+* the operator probes `divergence_term`, `gaussian_convolve`,
+  `tau_stability_bound`, `adaptive_lambda`, `diffusion_coefficient` ->
+  float64 kernels (csrc/pdz_ops.cu, pdz_frontend.cu);
+* the front end -> csrc/pdz_frontend.cu, pdz_guided.cu (bit-exact).
+
+numpy inputs return float64 numpy outputs like the reference; torch.cuda
+tensors stay on the device.  Precision: the solve iterates in float32 (the
+north-star contract: max-abs 1e-4 against the float64 reference at the
+stable step); see DESIGN.md for the documented deviations.
+"""
+
+from __future__ import annotations
+
+import csv
+import logging
+
+import numpy as np
+
+from . import _native as nat
+from .config import (ABLATIONS, LAMBDA_MODES, DehazeResult, SolverConfig, SolverTrace,
+                     normalize_ablation)
+from .image import (clamp01, is_device_array, to_device, to_host, validate_field,
+                    validate_image)
+from .refine import refine_dev
+from .scattering import _airlight_dev, _blend_weights, _dark_dev, _device_vec, _unit_range
+
+__all__ = [
+    "ABLATIONS",
+    "DehazeResult",
+    "SolverConfig",
+    "SolverTrace",
+    "adaptive_lambda",
+    "dehaze",
+    "dehaze_batch",
+    "diffusion_coefficient",
+    "divergence_term",
+    "fixed_point_solve",
+    "fixed_point_step",
+    "gaussian_convolve",
+    "gaussian_kernel",
+    "tau_stability_bound",
+    "write_trace_csv",
+    "DeviceProblem",
+    "prepare_problem",
+    "solve_problem",
+]
+
+# Same logger name as the reference module so existing log filters keep working
+# (the stability warning is asserted on "pdehaze.solver", tests/test_solver.py:126-131).
+logger = logging.getLogger("pdehaze.solver")
+
+
+def _params(h, w, planes, channels, cfg, *, edge_preserving=True, tau=None, max_iters=None,
+            rel_tol=None, kernel_size=None, sigma=None, epsilon=None) -> nat.SolveParams:
+    p = nat.SolveParams()
+    p.height, p.width, p.planes, p.channels = int(h), int(w), int(planes), int(channels)
+    p.kernel_size = int(cfg.kernel_size if kernel_size is None else kernel_size)
+    p.edge_preserving = 1 if edge_preserving else 0
+    p.max_iters = int(cfg.max_iters if max_iters is None else max_iters)
+    p.sigma = float(cfg.sigma if sigma is None else sigma)
+    p.epsilon = float(cfg.epsilon if epsilon is None else epsilon)
+    p.tau = float(cfg.tau if tau is None else tau)
+    p.rel_tol = float(cfg.rel_tol if rel_tol is None else rel_tol)
+    return p
+
+
+# --------------------------------------------------------------------------
+# operator probes (float64 kernels)
+# --------------------------------------------------------------------------
+
+def diffusion_coefficient(grad_magnitude, epsilon: float):
+    """D = 1 / (|grad| + epsilon), range (0, 1/eps] (solver.py:152-164)."""
+    import torch
+
+    scalar = np.isscalar(grad_magnitude)
+    g = grad_magnitude if is_device_array(grad_magnitude) else np.asarray(grad_magnitude,
+                                                                          dtype=np.float64)
+    if bool((g < 0.0).any()):
+        raise ValueError("gradient magnitude must be >= 0")
+    if epsilon <= 0.0:
+        raise ValueError("epsilon must be > 0")
+    g_dev = to_device(np.atleast_1d(g) if not is_device_array(g) else g, torch.float64)
+    out = torch.empty_like(g_dev)
+    nat.check(nat.lib().pdz_diffusion_coefficient(nat.ptr(g_dev), g_dev.numel(),
+                                                  float(epsilon), nat.ptr(out),
+                                                  nat.stream_ptr()))
+    if scalar:
+        return float(out.reshape(-1)[0].item())
+    res = to_host(out, grad_magnitude)
+    return res.reshape(np.shape(g)) if not is_device_array(grad_magnitude) else res
+
+
+def divergence_term(u, epsilon: float, edge_preserving: bool = True):
+    """div(D(grad u) grad u) with zero flux through the border (solver.py:190-210)."""
+    import torch
+
+    f = validate_field(u)
+    if f.shape[0] < 2 or f.shape[1] < 2:
+        raise ValueError(f"field must be at least 2x2, got {tuple(f.shape)}")
+    if epsilon <= 0.0:
+        raise ValueError("epsilon must be > 0")
+    f_dev = to_device(f, torch.float64)
+    out = torch.empty_like(f_dev)
+    prm = _params(f_dev.shape[0], f_dev.shape[1], 1, 1, SolverConfig(),
+                  edge_preserving=edge_preserving, epsilon=epsilon)
+    nat.check(nat.lib().pdz_divergence_f64(prm, nat.ptr(f_dev), nat.ptr(out), nat.stream_ptr()))
+    return to_host(out, u)
+
+
+def gaussian_kernel(sigma: float, kernel_size: int) -> np.ndarray:
+    """Sampled 2-D Gaussian normalised to sum 1 (solver.py:213-222): the outer
+    product of the library's normalised 1-D factor."""
+    if sigma <= 0.0:
+        raise ValueError("sigma must be > 0")
+    if kernel_size < 1 or kernel_size % 2 == 0:
+        raise ValueError(f"kernel_size must be odd and >= 1, got {kernel_size}")
+    taps = np.empty(kernel_size, dtype=np.float64)
+    nat.check(nat.lib().pdz_gaussian_taps(float(sigma), int(kernel_size), taps.ctypes.data))
+    return np.outer(taps, taps)
+
+
+def gaussian_convolve(field, sigma: float, kernel_size: int):
+    """Normalised Gaussian blur with symmetric (edge-inclusive) borders
+    (solver.py:225-241), evaluated separably."""
+    import torch
+
+    f = validate_field(field)
+    if sigma <= 0.0:
+        raise ValueError("sigma must be > 0")
+    if kernel_size < 1 or kernel_size % 2 == 0:
+        raise ValueError(f"kernel_size must be odd and >= 1, got {kernel_size}")
+    f_dev = to_device(f, torch.float64)
+    out = torch.empty_like(f_dev)
+    prm = _params(f_dev.shape[0], f_dev.shape[1], 1, 1, SolverConfig(), sigma=sigma,
+                  kernel_size=kernel_size)
+    lib = nat.lib()
+    ws = nat.workspace(lib.pdz_gaussian_workspace_bytes(prm, 1), "gauss")
+    nat.check(lib.pdz_gaussian_f64(prm, nat.ptr(f_dev), nat.ptr(out), nat.ptr(ws), ws.numel(),
+                                   nat.stream_ptr()))
+    return to_host(out, field)
+
+
+def adaptive_lambda(transmission, lambda0: float = 0.5, beta: float = 3.0,
+                    monotonicity: str = "as-printed"):
+    """lambda0 exp(-beta (1 - t)) ("as-printed") or lambda0 exp(-beta t)
+    ("prose") (solver.py:244-263)."""
+    import torch
+
+    t = validate_field(transmission)
+    if float(t.min()) < 0.0 or float(t.max()) > 1.0:
+        raise ValueError("transmission values must lie in [0, 1]")
+    if lambda0 <= 0.0:
+        raise ValueError("lambda0 must be > 0")
+    if beta < 0.0:
+        raise ValueError("beta must be >= 0")
+    if monotonicity not in LAMBDA_MODES:
+        raise ValueError(f"monotonicity must be one of {LAMBDA_MODES}")
+    t_dev = to_device(t, torch.float64)
+    out = torch.empty_like(t_dev)
+    nat.check(nat.lib().pdz_adaptive_lambda(nat.ptr(t_dev), t_dev.numel(),
+                                            nat.LAMBDA_MODES_C[monotonicity], float(lambda0),
+                                            float(beta), nat.ptr(out), nat.stream_ptr()))
+    return to_host(out, transmission)
+
+
+def tau_stability_bound(u, lambda_map, epsilon: float) -> float:
+    """2 / (8 max D + max(max lambda, 0)), D edge-preserving (solver.py:266-277)."""
+    import torch
+
+    f = validate_field(u)
+    lam = validate_field(lambda_map)
+    f_dev = to_device(f, torch.float64)
+    if tuple(lam.shape) == tuple(f.shape):
+        lam_dev = to_device(lam, torch.float64)
+        lam_extra = None
+    else:  # the reference reduces the two fields independently
+        lam_dev = torch.zeros_like(f_dev)
+        lam_extra = float(lam.max())
+    prm = _params(f_dev.shape[0], f_dev.shape[1], 1, 1, SolverConfig(), epsilon=epsilon)
+    lib = nat.lib()
+    ws = nat.workspace(lib.pdz_tau_bound_workspace_bytes(prm), "tau")
+    bound = torch.empty(1, dtype=torch.float64, device=f_dev.device)
+    nat.check(lib.pdz_tau_bound_f64(prm, nat.ptr(f_dev), nat.ptr(lam_dev), nat.ptr(bound),
+                                    nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+    b = float(bound.item())
+    if lam_extra is not None:
+        max_d = (2.0 / b) / 8.0
+        b = 2.0 / (8.0 * max_d + max(lam_extra, 0.0))
+    return b
+
+
+# --------------------------------------------------------------------------
+# the sweep
+# --------------------------------------------------------------------------
+
+def fixed_point_step(u, source, lambda_map, cfg: SolverConfig, *, edge_preserving: bool = True,
+                     tau: float | None = None):
+    """One relaxed update (u + tau r, ||r||_2), r = div(D grad u) - lambda G(u) +
+    source (solver.py:280-302), on the fused float32 sweep kernel."""
+    import torch
+
+    uu = validate_field(u)
+    src = validate_field(source)
+    lam = validate_field(lambda_map)
+    if tuple(uu.shape) != tuple(src.shape) or tuple(uu.shape) != tuple(lam.shape):
+        raise ValueError(f"shape mismatch: u {tuple(uu.shape)}, source {tuple(src.shape)}, "
+                         f"lambda {tuple(lam.shape)}")
+    step = cfg.tau if tau is None else float(tau)
+    h, w = uu.shape
+    u_dev = to_device(uu, torch.float32)
+    s_dev = to_device(src, torch.float32)
+    l_dev = to_device(lam, torch.float32)
+    out = torch.empty_like(u_dev)
+    prm = _params(h, w, 1, 1, cfg, edge_preserving=edge_preserving, tau=step, max_iters=1)
+    lib = nat.lib()
+    ws = nat.workspace(lib.pdz_step_workspace_bytes(prm), "step")
+    norms = torch.empty(1, dtype=torch.float64, device=u_dev.device)
+    nat.check(lib.pdz_fixed_point_step(prm, nat.ptr(u_dev), nat.ptr(out), nat.ptr(s_dev),
+                                       nat.ptr(l_dev), nat.ptr(norms), None, nat.ptr(ws),
+                                       ws.numel(), nat.stream_ptr()))
+    norm = float(norms.item())
+    if step == 0.0:
+        # u + 0 * r is u itself; keep the caller's values bit-for-bit
+        # (the float32 iterate would round them).
+        return (uu.clone() if is_device_array(uu) else np.array(uu, dtype=np.float64)), norm
+    return to_host(out.to(torch.float64) if not is_device_array(u) else out, u), norm
+
+
+class DeviceProblem:
+    """Device-resident solver inputs for P = batch * C planes of H x W."""
+
+    def __init__(self, phi, lam, height, width, planes, channels):
+        self.phi = phi          # float32 [P][H][W]
+        self.lam = lam          # float32 [P/C][H][W]
+        self.height = height
+        self.width = width
+        self.planes = planes
+        self.channels = channels
+
+
+def _tau_bounds(problem: DeviceProblem, cfg, epsilon) -> np.ndarray:
+    import torch
+
+    prm = _params(problem.height, problem.width, problem.planes, problem.channels, cfg,
+                  epsilon=epsilon)
+    lib = nat.lib()
+    ws = nat.workspace(lib.pdz_tau_bound_workspace_bytes(prm), "tau")
+    out = torch.empty(problem.planes, dtype=torch.float64, device=problem.phi.device)
+    nat.check(lib.pdz_tau_bound(prm, nat.ptr(problem.phi), nat.ptr(problem.lam), nat.ptr(out),
+                                nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+    return out.to("cpu").numpy()
+
+
+def solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=True,
+                  tau=None, warn=True):
+    """fixed_point_solve for every plane at once.  Returns (u [P][H][W] float32
+    device tensor, [SolverTrace] * P)."""
+    import torch
+
+    step = cfg.tau if tau is None else float(tau)
+    bounds = _tau_bounds(problem, cfg, cfg.epsilon)
+    if warn:
+        for b in bounds:
+            if step > b:
+                logger.warning(
+                    "relaxation step %.3g exceeds the stability bound %.3g at the "
+                    "initial iterate; convergence is not guaranteed", step, b)
+    P = problem.planes
+    prm = _params(problem.height, problem.width, P, problem.channels, cfg,
+                  edge_preserving=edge_preserving, tau=step)
+    lib = nat.lib()
+    ws = nat.workspace(lib.pdz_solve_workspace_bytes(prm), "solve")
+    u = torch.empty_like(problem.phi)
+    norms = np.zeros((cfg.max_iters, P), dtype=np.float64)
+    iters = np.zeros(P, dtype=np.int32)
+    conv = np.zeros(P, dtype=np.int32)
+    failed = np.zeros(P, dtype=np.int32)
+    rc = lib.pdz_fixed_point_solve(prm, nat.ptr(problem.phi), nat.ptr(problem.lam), nat.ptr(u),
+                                   norms.ctypes.data, iters.ctypes.data, conv.ctypes.data,
+                                   failed.ctypes.data, nat.ptr(ws), ws.numel(),
+                                   nat.stream_ptr())
+    if rc == nat.PDZ_ENONFINITE:
+        first = int(np.flatnonzero(failed)[0])
+        raise FloatingPointError(
+            f"solver produced non-finite values at iteration {int(failed[first])}")
+    nat.check(rc)
+    traces = []
+    for p in range(P):
+        n = int(iters[p])
+        traces.append(SolverTrace(residual_norms=[float(v) for v in norms[:n, p]],
+                                  iterations_run=n, converged=bool(conv[p]), tau_used=step,
+                                  tau_bound=float(bounds[p])))
+    return u, traces
+
+
+def _lambda_mode(flags, cfg) -> int:
+    if "no-nonlocal" in flags:
+        return nat.LAMBDA_MODES_C["zero"]
+    if "no-adaptive" in flags:
+        return nat.LAMBDA_MODES_C["const"]
+    return nat.LAMBDA_MODES_C[cfg.lambda_monotonicity]
+
+
+def prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, lambda_mode, phi=None, lam=None):
+    """Phi planes and lambda for one image straight from the device front end."""
+    import torch
+
+    h, w, c = img_dev.shape
+    if phi is None:
+        phi = torch.empty((c, h, w), dtype=torch.float32, device=img_dev.device)
+    if lam is None:
+        lam = torch.empty((h, w), dtype=torch.float32, device=img_dev.device)
+    nat.check(nat.lib().pdz_solver_fields(nat.ptr(img_dev), is_f64, h, w, c, nat.ptr(t_dev),
+                                          nat.ptr(a_dev), float(cfg.t_floor), int(lambda_mode),
+                                          float(cfg.lambda0), float(cfg.beta), nat.ptr(phi),
+                                          nat.ptr(lam), None, nat.stream_ptr()))
+    return phi, lam
+
+
+def fixed_point_solve(channel, transmission, airlight_c: float, cfg: SolverConfig, *,
+                      lambda_map=None, edge_preserving: bool = True, tau: float | None = None):
+    """Relaxed fixed-point solve of one channel from u0 = Phi with the
+    relative residual-change stop rule (solver.py:305-359).  Returns
+    (u unclamped, SolverTrace)."""
+    import torch
+
+    ch = validate_field(channel)
+    t = validate_field(transmission)
+    if tuple(t.shape) != tuple(ch.shape):
+        raise ValueError(f"transmission shape {tuple(t.shape)} != channel shape "
+                         f"{tuple(ch.shape)}")
+    if not 0.0 < airlight_c <= 1.0:
+        raise ValueError("per-channel airlight must lie in (0, 1]")
+    if float(t.min()) < 0.0 or float(t.max()) > 1.0:
+        raise ValueError("transmission values must lie in [0, 1]")
+    lam_given = None
+    if lambda_map is not None:
+        lam_given = validate_field(lambda_map)
+        if tuple(lam_given.shape) != tuple(ch.shape):
+            raise ValueError(f"lambda map shape {tuple(lam_given.shape)} != channel shape "
+                             f"{tuple(ch.shape)}")
+    h, w = ch.shape
+    img_dev = to_device(ch, torch.float64).reshape(h, w, 1)
+    t_dev = to_device(t, torch.float64)
+    a_dev = _device_vec(np.array([float(airlight_c)]))
+    phi, lam = prepare_problem(img_dev, 1, t_dev, a_dev, cfg,
+                               nat.LAMBDA_MODES_C[cfg.lambda_monotonicity])
+    if lam_given is not None:
+        lam = to_device(lam_given, torch.float32).reshape(h, w)
+    problem = DeviceProblem(phi, lam, h, w, 1, 1)
+    u, traces = solve_problem(problem, cfg, edge_preserving=edge_preserving, tau=tau)
+    out = u[0]
+    if not is_device_array(channel):
+        out = out.to(torch.float64).to("cpu").numpy()
+    return out, traces[0]
+
+
+# --------------------------------------------------------------------------
+# the pipeline
+# --------------------------------------------------------------------------
+
+def _front_end(img_dev, is_f64, cfg, flags):
+    """dark (A = 1) -> airlight -> normalised dark -> t -> guided refinement
+    (solver.py:393-408), all on the device.  Returns (t_dev, a_dev)."""
+    import torch
+
+    h, w, c = img_dev.shape
+    if "no-multiscale" in flags:
+        radii, weights = (cfg.patch_radius,), (1.0,)
+    else:
+        radii, weights = _blend_weights(cfg.multiscale_radii, cfg.multiscale_weights)
+    if any(r < 0 for r in radii):
+        raise ValueError("patch_radius must be >= 0")
+    ones = torch.ones(c, dtype=torch.float64, device=img_dev.device)
+    dark = torch.empty((h, w), dtype=torch.float64, device=img_dev.device)
+    _dark_dev(img_dev, is_f64, ones, radii, weights, dark)
+    a_dev, _ = _airlight_dev(img_dev, is_f64, dark, cfg.airlight_fraction)
+    _dark_dev(img_dev, is_f64, a_dev, radii, weights, dark)
+    t_dev = torch.empty_like(dark)
+    nat.check(nat.lib().pdz_transmission(nat.ptr(dark), h, w, float(cfg.omega), nat.ptr(t_dev),
+                                         nat.stream_ptr()))
+    if "no-guided" not in flags:
+        t_dev = refine_dev(img_dev, is_f64, t_dev, cfg.guided_radius, cfg.guided_reg)
+    return t_dev, a_dev
+
+
+def _image_dev(img):
+    import torch
+
+    t = to_device(img)
+    return t, 1 if t.dtype == torch.float64 else 0
+
+
+def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1):
+    """Full pipeline (solver.py:375-436): front end -> per-channel relaxed
+    solve (all channels in one fused sweep per iteration) -> clamp.  `workers`
+    is accepted for compatibility; the output does not depend on it."""
+    import torch
+
+    cfg = cfg or SolverConfig()
+    flags = normalize_ablation(ablation)
+    # torch inputs (pinned host or device) are moved first and validated on the GPU
+    img = validate_image(to_device(image) if is_device_array(image) else image)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    _unit_range(img)
+    img_dev, is_f64 = _image_dev(img)
+    h, w, c = img_dev.shape
+    t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
+    lib = nat.lib()
+    if "no-pde" in flags:
+        phi64 = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
+        nat.check(lib.pdz_solver_fields(nat.ptr(img_dev), is_f64, h, w, c, nat.ptr(t_dev),
+                                        nat.ptr(a_dev), float(cfg.t_floor), 0, 0.5, 3.0, None,
+                                        None, nat.ptr(phi64), nat.stream_ptr()))
+        out = clamp01(phi64)
+        return (to_host(out, image),
+                DehazeResult(to_host(a_dev, image), to_host(t_dev, image), [], flags))
+    if h < 2 or w < 2:
+        raise ValueError(f"field must be at least 2x2, got {(h, w)}")
+    phi, lam = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg))
+    problem = DeviceProblem(phi, lam, h, w, c, c)
+    u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
+    nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1, nat.stream_ptr()))
+    return (to_host(out, image),
+            DehazeResult(to_host(a_dev, image), to_host(t_dev, image), traces, flags))
+
+
+def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
+    """Extension for batched serving (BASELINE config 3): same results as
+    calling `dehaze` on each image, but every image's planes are swept by one
+    launch per iteration.  `images`: (B, H, W, C) array or sequence of equal-
+    shaped images.  Returns (restored (B, H, W, C), [DehazeResult] * B)."""
+    import torch
+
+    cfg = cfg or SolverConfig()
+    flags = normalize_ablation(ablation)
+    if "no-pde" in flags:
+        outs = [dehaze(im, cfg, ablation) for im in images]
+        return np.stack([o for o, _ in outs]), [r for _, r in outs]
+    batch = [validate_image(im) for im in images]
+    if not batch:
+        raise ValueError("images must be nonempty")
+    shape = tuple(batch[0].shape)
+    if any(tuple(b.shape) != shape for b in batch):
+        raise ValueError("all images of a batch must share one shape")
+    h, w, c = shape
+    if h < 2 or w < 2:
+        raise ValueError(f"field must be at least 2x2, got {(h, w)}")
+    B = len(batch)
+    dev = nat.device()
+    phi = torch.empty((B * c, h, w), dtype=torch.float32, device=dev)
+    lam = torch.empty((B, h, w), dtype=torch.float32, device=dev)
+    fronts = []
+    for i, im in enumerate(batch):
+        _unit_range(im)
+        img_dev, is_f64 = _image_dev(im)
+        t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
+        prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
+                        phi=phi[i * c:(i + 1) * c], lam=lam[i])
+        fronts.append((t_dev, a_dev))
+    problem = DeviceProblem(phi, lam, h, w, B * c, c)
+    u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
+    lib = nat.lib()
+    for i in range(B):
+        nat.check(lib.pdz_clamp_interleave(nat.ptr(u[i * c:(i + 1) * c]), h, w, c,
+                                           nat.ptr(out[i]), 1, nat.stream_ptr()))
+    host = not is_device_array(images if not isinstance(images, (list, tuple)) else images[0])
+    results = []
+    for i, (t_dev, a_dev) in enumerate(fronts):
+        results.append(DehazeResult(a_dev.cpu().numpy() if host else a_dev,
+                                    t_dev.cpu().numpy() if host else t_dev,
+                                    traces[i * c:(i + 1) * c], flags))
+    return (out.cpu().numpy() if host else out), results
+
+
+def write_trace_csv(traces, path) -> None:
+    """CSV rows (channel, iteration, residual_norm) with repr() norms
+    (solver.py:439-446)."""
+    with open(path, "w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(["channel", "iteration", "residual_norm"])
+        for channel, trace in enumerate(traces):
+            for iteration, norm in enumerate(trace.residual_norms, start=1):
+                writer.writerow([channel, iteration, repr(norm)])
+
