@@ -153,6 +153,11 @@ int32_t pdz_diffusion_coefficient(const double* grad_magnitude, int64_t n, doubl
 size_t pdz_tau_bound_workspace_bytes(const pdz_solve_params* params);
 int32_t pdz_tau_bound(const pdz_solve_params* params, const float* u, const float* lambda_map,
                       double* bound, void* workspace, size_t workspace_bytes, void* stream);
+/* Same bound from a float64 interleaved [H][W][C] iterate (the float64 Phi of
+ * pdz_solver_fields) and the float32 lambda plane; planes == channels. */
+int32_t pdz_tau_bound_hwc(const pdz_solve_params* params, const double* u_hwc,
+                          const float* lambda_map, double* bound, void* workspace,
+                          size_t workspace_bytes, void* stream);
 int32_t pdz_tau_bound_f64(const pdz_solve_params* params, const double* u,
                           const double* lambda_map, double* bound, void* workspace,
                           size_t workspace_bytes, void* stream);

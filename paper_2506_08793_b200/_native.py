@@ -80,6 +80,7 @@ _SIGNATURES = {
     "pdz_tau_bound_workspace_bytes": (_sz, [_pp]),
     "pdz_tau_bound": (_i32, [_pp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_tau_bound_f64": (_i32, [_pp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "pdz_tau_bound_hwc": (_i32, [_pp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_divergence": (_i32, [_pp, _vp, _vp, _vp]),
     "pdz_divergence_f64": (_i32, [_pp, _vp, _vp, _vp]),
     "pdz_gaussian_workspace_bytes": (_sz, [_pp, _i32]),

@@ -93,38 +93,42 @@ __global__ void tau_init_kernel(unsigned long long* smin, unsigned long long* lm
   }
 }
 
-template <typename T>
-__global__ void tau_scan_kernel(const T* __restrict__ u, const T* __restrict__ lam, int H, int W,
-                                int C, unsigned long long* smin, unsigned long long* lmax) {
+// u: sample (y, x) of plane p at u[p*ps + (y*W + x)*us] (planar: us = 1,
+// ps = H*W; interleaved [H][W][C]: us = C, ps = 1).  lambda planar [P/C][H][W].
+template <typename TU, typename TL>
+__global__ void tau_scan_kernel(const TU* __restrict__ u, const TL* __restrict__ lam, int H,
+                                int W, int C, size_t us, size_t ps, unsigned long long* smin,
+                                unsigned long long* lmax) {
   const int p = blockIdx.y;
-  const T* f = u + size_t(p) * H * W;
-  const T* lp = lam + size_t(p / C) * H * W;
+  const TU* f = u + size_t(p) * ps;
+  const TL* lp = lam + size_t(p / C) * H * W;
   double best = INFINITY;
   double lbest = -INFINITY;
   const size_t n = size_t(H) * W;
+  auto at = [&](size_t j) -> double { return double(f[j * us]); };
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
     const int y = int(i / W), x = int(i - size_t(y) * W);
-    const double c = double(f[i]);
+    const double c = at(i);
     auto cy = [&](int xx) -> double {
       const size_t j = size_t(y) * W + xx;
-      if (y == 0) return double(f[j + W]) - double(f[j]);
-      if (y == H - 1) return double(f[j]) - double(f[j - W]);
-      return (double(f[j + W]) - double(f[j - W])) / 2.0;
+      if (y == 0) return at(j + W) - at(j);
+      if (y == H - 1) return at(j) - at(j - W);
+      return (at(j + W) - at(j - W)) / 2.0;
     };
     auto cx = [&](int yy) -> double {
       const size_t j = size_t(yy) * W + x;
-      if (x == 0) return double(f[j + 1]) - double(f[j]);
-      if (x == W - 1) return double(f[j]) - double(f[j - 1]);
-      return (double(f[j + 1]) - double(f[j - 1])) / 2.0;
+      if (x == 0) return at(j + 1) - at(j);
+      if (x == W - 1) return at(j) - at(j - 1);
+      return (at(j + 1) - at(j - 1)) / 2.0;
     };
     if (x < W - 1) {
-      const double jump = double(f[i + 1]) - c;
+      const double jump = at(i + 1) - c;
       const double along = 0.5 * (cy(x + 1) + cy(x));
       best = fmin(best, jump * jump + along * along);
     }
     if (y < H - 1) {
-      const double jump = double(f[i + W]) - c;
+      const double jump = at(i + W) - c;
       const double along = 0.5 * (cx(y + 1) + cx(y));
       best = fmin(best, jump * jump + along * along);
     }
@@ -216,9 +220,9 @@ static int32_t run_gaussian(const pdz_solve_params* prm, const T* u, T* out, voi
   return cudaStreamSynchronize(s) == cudaSuccess ? PDZ_OK : cuda_status(cudaGetLastError(), "gaussian sync");
 }
 
-template <typename T>
-static int32_t run_tau(const pdz_solve_params* prm, const T* u, const T* lam, double* bound,
-                       void* ws, size_t ws_bytes, void* stream) {
+template <typename TU, typename TL>
+static int32_t run_tau(const pdz_solve_params* prm, const TU* u, const TL* lam, double* bound,
+                       void* ws, size_t ws_bytes, void* stream, bool interleaved = false) {
   PDZ_REQUIRE(prm && u && lam && bound, "NULL argument");
   PDZ_REQUIRE(prm->height >= 2 && prm->width >= 2, "field must be at least 2x2, got (%d, %d)",
               prm->height, prm->width);
@@ -237,8 +241,9 @@ static int32_t run_tau(const pdz_solve_params* prm, const T* u, const T* lam, do
   tau_init_kernel<<<(P + 255) / 256, 256, 0, s>>>(smin, lmax, P);
   const size_t n = size_t(prm->height) * prm->width;
   const int bx = int(std::min<size_t>((n + 255) / 256, size_t(4 * num_sms())));
-  tau_scan_kernel<T><<<dim3(bx, P), 256, 0, s>>>(u, lam, prm->height, prm->width,
-                                                 prm->channels, smin, lmax);
+  const size_t us = interleaved ? size_t(P) : 1, ps = interleaved ? 1 : n;
+  tau_scan_kernel<TU, TL><<<dim3(bx, P), 256, 0, s>>>(u, lam, prm->height, prm->width,
+                                                      prm->channels, us, ps, smin, lmax);
   tau_final_kernel<<<(P + 255) / 256, 256, 0, s>>>(smin, lmax, P, prm->channels,
                                                    prm->epsilon, bound);
   PDZ_CHECK_LAUNCH("tau bound");
@@ -282,12 +287,23 @@ size_t pdz_tau_bound_workspace_bytes(const pdz_solve_params* params) {
 }
 int32_t pdz_tau_bound(const pdz_solve_params* params, const float* u, const float* lambda_map,
                       double* bound, void* workspace, size_t workspace_bytes, void* stream) {
-  return run_tau<float>(params, u, lambda_map, bound, workspace, workspace_bytes, stream);
+  return run_tau<float, float>(params, u, lambda_map, bound, workspace, workspace_bytes, stream);
 }
 int32_t pdz_tau_bound_f64(const pdz_solve_params* params, const double* u,
                           const double* lambda_map, double* bound, void* workspace,
                           size_t workspace_bytes, void* stream) {
-  return run_tau<double>(params, u, lambda_map, bound, workspace, workspace_bytes, stream);
+  return run_tau<double, double>(params, u, lambda_map, bound, workspace, workspace_bytes,
+                                 stream);
+}
+int32_t pdz_tau_bound_hwc(const pdz_solve_params* params, const double* u_hwc,
+                          const float* lambda_map, double* bound, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  if (params && params->planes != params->channels) {
+    set_error("pdz_tau_bound_hwc handles one image (planes == channels)");
+    return PDZ_EINVAL;
+  }
+  return run_tau<double, float>(params, u_hwc, lambda_map, bound, workspace, workspace_bytes,
+                                stream, true);
 }
 
 }  // extern "C"

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
   const int SW = kTW + 2 * R;
   const int PU = SW + 1;  // odd pitch: conflict-free row-group access
   float* s_u = smem;                  // [SH][PU] iterate tile + halo
-  float* s_h = smem + SH * PU;        // [SH][kTW] horizontally blurred rows
+  float* s_h = smem + ((SH * PU + 3) & ~3);  // [SH][kTW] horizontally blurred rows (16B aligned)
   __shared__ double s_red[kThreads / 32];
   __shared__ int s_nf[kThreads / 32];
 
@@ -355,7 +355,7 @@ static SweepFn prepared() {
   static bool done = false;
   if (!done) {
     const int R = RT >= 0 ? RT : kMaxFusedRadius;
-    const size_t smem = size_t((kTH + 2 * R) * (kTW + 2 * R + 1) + (kTH + 2 * R) * kTW) * 4;
+    const size_t smem = size_t(((kTH + 2 * R) * (kTW + 2 * R + 1) + 3 + (kTH + 2 * R) * kTW)) * 4;
     cudaFuncSetAttribute(sweep_kernel<RT, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
     done = true;
@@ -378,7 +378,7 @@ static SweepFn pick_kernel(int R) {
 }
 
 static size_t sweep_smem(int R) {
-  return size_t((kTH + 2 * R) * (kTW + 2 * R + 1) + (kTH + 2 * R) * kTW) * 4;
+  return size_t(((kTH + 2 * R) * (kTW + 2 * R + 1) + 3 + (kTH + 2 * R) * kTW)) * 4;
 }
 
 struct Geometry {

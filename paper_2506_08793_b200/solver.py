@@ -238,13 +238,17 @@ def fixed_point_step(u, source, lambda_map, cfg: SolverConfig, *, edge_preservin
 class DeviceProblem:
     """Device-resident solver inputs for P = batch * C planes of H x W."""
 
-    def __init__(self, phi, lam, height, width, planes, channels):
+    def __init__(self, phi, lam, height, width, planes, channels, bounds=None):
         self.phi = phi          # float32 [P][H][W]
         self.lam = lam          # float32 [P/C][H][W]
         self.height = height
         self.width = width
         self.planes = planes
         self.channels = channels
+        # tau_stability_bound per plane at u0 = Phi, from the float64 Phi when
+        # the front end produced it (float32 Phi shifts the minimum face
+        # gradient of near-flat regions by ~1e-6 relative)
+        self.bounds = bounds
 
 
 def _tau_bounds(problem: DeviceProblem, cfg, epsilon) -> np.ndarray:
@@ -267,7 +271,8 @@ def solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=
     import torch
 
     step = cfg.tau if tau is None else float(tau)
-    bounds = _tau_bounds(problem, cfg, cfg.epsilon)
+    bounds = problem.bounds if problem.bounds is not None else _tau_bounds(problem, cfg,
+                                                                          cfg.epsilon)
     if warn:
         for b in bounds:
             if step > b:
@@ -310,8 +315,11 @@ def _lambda_mode(flags, cfg) -> int:
     return nat.LAMBDA_MODES_C[cfg.lambda_monotonicity]
 
 
-def prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, lambda_mode, phi=None, lam=None):
-    """Phi planes and lambda for one image straight from the device front end."""
+def prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, lambda_mode, phi=None, lam=None,
+                    with_bounds=False, lam_override=None):
+    """Phi planes and lambda for one image straight from the device front end.
+    With `with_bounds`, also returns the per-channel tau_stability_bound at
+    u0 = Phi evaluated on the float64 Phi (solver.py:334)."""
     import torch
 
     h, w, c = img_dev.shape
@@ -319,11 +327,25 @@ def prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, lambda_mode, phi=None, l
         phi = torch.empty((c, h, w), dtype=torch.float32, device=img_dev.device)
     if lam is None:
         lam = torch.empty((h, w), dtype=torch.float32, device=img_dev.device)
-    nat.check(nat.lib().pdz_solver_fields(nat.ptr(img_dev), is_f64, h, w, c, nat.ptr(t_dev),
-                                          nat.ptr(a_dev), float(cfg.t_floor), int(lambda_mode),
-                                          float(cfg.lambda0), float(cfg.beta), nat.ptr(phi),
-                                          nat.ptr(lam), None, nat.stream_ptr()))
-    return phi, lam
+    phi64 = (torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
+             if with_bounds else None)
+    lib = nat.lib()
+    nat.check(lib.pdz_solver_fields(nat.ptr(img_dev), is_f64, h, w, c, nat.ptr(t_dev),
+                                    nat.ptr(a_dev), float(cfg.t_floor), int(lambda_mode),
+                                    float(cfg.lambda0), float(cfg.beta), nat.ptr(phi),
+                                    nat.ptr(lam), nat.ptr(phi64), nat.stream_ptr()))
+    if lam_override is not None:
+        lam.copy_(lam_override)
+    if not with_bounds:
+        return phi, lam
+    if h < 2 or w < 2:
+        raise ValueError(f"field must be at least 2x2, got {(h, w)}")
+    prm = _params(h, w, c, c, cfg)
+    ws = nat.workspace(lib.pdz_tau_bound_workspace_bytes(prm), "tau")
+    bounds = torch.empty(c, dtype=torch.float64, device=img_dev.device)
+    nat.check(lib.pdz_tau_bound_hwc(prm, nat.ptr(phi64), nat.ptr(lam), nat.ptr(bounds),
+                                    nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+    return phi, lam, bounds.to("cpu").numpy()
 
 
 def fixed_point_solve(channel, transmission, airlight_c: float, cfg: SolverConfig, *,
@@ -352,11 +374,11 @@ def fixed_point_solve(channel, transmission, airlight_c: float, cfg: SolverConfi
     img_dev = to_device(ch, torch.float64).reshape(h, w, 1)
     t_dev = to_device(t, torch.float64)
     a_dev = _device_vec(np.array([float(airlight_c)]))
-    phi, lam = prepare_problem(img_dev, 1, t_dev, a_dev, cfg,
-                               nat.LAMBDA_MODES_C[cfg.lambda_monotonicity])
-    if lam_given is not None:
-        lam = to_device(lam_given, torch.float32).reshape(h, w)
-    problem = DeviceProblem(phi, lam, h, w, 1, 1)
+    override = None if lam_given is None else to_device(lam_given, torch.float32).reshape(h, w)
+    phi, lam, bounds = prepare_problem(img_dev, 1, t_dev, a_dev, cfg,
+                                       nat.LAMBDA_MODES_C[cfg.lambda_monotonicity],
+                                       with_bounds=True, lam_override=override)
+    problem = DeviceProblem(phi, lam, h, w, 1, 1, bounds)
     u, traces = solve_problem(problem, cfg, edge_preserving=edge_preserving, tau=tau)
     out = u[0]
     if not is_device_array(channel):
@@ -427,8 +449,9 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
                 DehazeResult(to_host(a_dev, image), to_host(t_dev, image), [], flags))
     if h < 2 or w < 2:
         raise ValueError(f"field must be at least 2x2, got {(h, w)}")
-    phi, lam = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg))
-    problem = DeviceProblem(phi, lam, h, w, c, c)
+    phi, lam, bounds = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg,
+                                       _lambda_mode(flags, cfg), with_bounds=True)
+    problem = DeviceProblem(phi, lam, h, w, c, c, bounds)
     u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
     nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1, nat.stream_ptr()))
@@ -461,15 +484,16 @@ def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
     dev = nat.device()
     phi = torch.empty((B * c, h, w), dtype=torch.float32, device=dev)
     lam = torch.empty((B, h, w), dtype=torch.float32, device=dev)
-    fronts = []
+    fronts, bounds = [], []
     for i, im in enumerate(batch):
         _unit_range(im)
         img_dev, is_f64 = _image_dev(im)
         t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
-        prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
-                        phi=phi[i * c:(i + 1) * c], lam=lam[i])
+        _, _, b = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
+                                  phi=phi[i * c:(i + 1) * c], lam=lam[i], with_bounds=True)
         fronts.append((t_dev, a_dev))
-    problem = DeviceProblem(phi, lam, h, w, B * c, c)
+        bounds.append(b)
+    problem = DeviceProblem(phi, lam, h, w, B * c, c, np.concatenate(bounds))
     u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
     lib = nat.lib()
