@@ -212,6 +212,9 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
 /* Number of kernels pdz_fixed_point_sweeps_async launches for `params`
  * (benchmark bookkeeping). */
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);
+/* Which sweep kernel `params` runs on: 2 = streaming (width % 4 == 0 and a
+ * compiled radius), 1 = tiled fallback, -1 = invalid params. */
+int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params);
 /* Device pointer to the plane-p final iterate inside a solve workspace after
  * pdz_fixed_point_sweeps_async (buffer parity of `iterations`). */
 const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* workspace,

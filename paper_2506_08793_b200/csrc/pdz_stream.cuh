@@ -1,0 +1,480 @@
+// Streaming relaxed fixed-point sweep (v2) -- the production hot kernel.
+//
+// Same mathematics as the tiled sweep (pdz_sweep.cu; solver.py:280-302), laid
+// out for B200:
+//  * persistent CTAs (one or two per SM); CTA i owns the exactly balanced
+//    range [floor(iS/G), floor((i+1)S/G)) of the S = planes x strips x H
+//    "strip-rows" (strip = 64 output columns), so every SM gets the same
+//    number of pixels (+-1 row) -- no wave quantisation on 148 SMs;
+//  * each CTA streams down its strip in blocks of 64 rows; input rows (64 +
+//    2*ceil4(R) columns) arrive by cp.async.bulk (TMA bulk copies, UBLKCP)
+//    into a double buffer, signalled by an mbarrier, while the previous block
+//    computes; the horizontally blurred rows of the 2R-row overlap are carried
+//    from block to block instead of recomputed (only segment starts pay the
+//    vertical halo);
+//  * horizontal Gaussian pass from shared memory (4 outputs per item),
+//    vertical pass with packed FFMA2 (fma.rn.f32x2) over column pairs,
+//    face fluxes with MUFU sqrt/rcp, residual, update and r^2 fused in
+//    registers; Phi/lambda prefetched into registers before the block waits;
+//  * warps 0-7 compute; warp 8 is a service warp: in CTA 0 it reduces the
+//    previous iteration's norm partials and applies the stop rule
+//    concurrently with the sweep (no serial tail, no extra launch).
+// Border handling: rows are reflected (np.pad "symmetric", solver.py:235) at
+// load time; out-of-image columns are fixed up in shared memory from their
+// reflected in-window sources; the centred differences use the one-sided
+// form at the first/last row/column (np.gradient, solver.py:178-179).
+// Requirements: width % 4 == 0 (16-byte bulk copies) and a compiled radius;
+// other shapes use the tiled kernel.
+#pragma once
+#include <algorithm>
+#include <cmath>
+
+#include "pdz_solver.cuh"
+
+namespace pdz {
+
+constexpr int kSTW = 64;                   // strip width (output columns)
+constexpr int kSRB = 64;                   // output rows per block
+constexpr int kSCW = 8;                    // compute warps
+constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
+constexpr int kComputeThreads = kSCW * 32;
+
+template <int R>
+struct SGeo {
+  static constexpr int RP = (R + 3) & ~3;        // column halo rounded to float4
+  static constexpr int PWD = kSTW + 2 * RP;      // staged floats per row
+  static constexpr int PITCH = (PWD + 31) & ~31;  // 128-byte aligned smem rows
+  static constexpr int ROWS = kSRB + 2 * R;      // staged input rows / H rows
+  static constexpr int IN_FLOATS = ROWS * PITCH;
+  static constexpr int H_FLOATS = ROWS * kSTW;
+  static constexpr size_t SMEM = size_t(2 * IN_FLOATS + 2 * H_FLOATS) * 4 + 128;
+};
+
+struct StreamArgs {
+  float* buf0;
+  float* buf1;
+  const float* phi;
+  const float* lam;
+  Partials pt;
+  StateView st;  // st.stop_iter == nullptr: single step
+  int32_t H, W, P, C, nstrips;
+  int32_t iter_off, max_iters;
+  float eps, tau;
+  double rel_tol;
+  float w[kMaxTaps];
+};
+
+// ------------------------------------------------------------ primitives --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// Bulk global -> shared copy (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void compute_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// d = a * b + c on packed float pairs (FFMA2).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+template <bool EDGE>
+__device__ __forceinline__ float sflux(float jump, float along, float eps) {
+  if (!EDGE) return jump;
+  const float s = fmaf(jump, jump, along * along);
+  return jump * rcp_approx(sqrt_approx(s) + eps);
+}
+
+struct SBlock {
+  int p, x0, yb, n, first;
+};
+
+// Next block of this CTA's range; skips planes frozen at <= iter-2.
+__device__ __forceinline__ bool next_block(int64_t& L, int64_t L0, int64_t L1,
+                                           const StreamArgs& a, int iter, SBlock& b) {
+  while (L < L1) {
+    const int64_t u = L / a.H;
+    const int y = int(L - u * a.H);
+    const int64_t seg_end = min(L1, (u + 1) * int64_t(a.H));
+    const int p = int(u / a.nstrips);
+    if (a.st.stop_iter) {
+      const int s = a.st.stop_iter[p];
+      if (s != 0 && s < iter - 1) {
+        L = seg_end;
+        continue;
+      }
+    }
+    b.p = p;
+    b.x0 = int(u - int64_t(p) * a.nstrips) * kSTW;
+    b.yb = y;
+    b.n = int(seg_end - L < kSRB ? seg_end - L : int64_t(kSRB));
+    b.first = (L == L0) || (y == 0);
+    L += b.n;
+    return true;
+  }
+  return false;
+}
+
+// Warp 0 of the compute warps: queue the bulk copies of the block's new input
+// rows (reflected row indices, in-image column span) into `in`.
+template <int R>
+__device__ __forceinline__ void issue_rows(const SBlock& b, const float* __restrict__ uin,
+                                           float* in, uint64_t* bar, int H, int W, int lane) {
+  using Gm = SGeo<R>;
+  const int r0 = b.first ? b.yb - R : b.yb + R;
+  const int nrows = b.first ? b.n + 2 * R : b.n;
+  const int idx0 = b.first ? 0 : R + 1;
+  const int gc0 = max(0, b.x0 - Gm::RP);
+  const int gc1 = min(W, b.x0 + kSTW + Gm::RP);
+  const uint32_t bytes = uint32_t(gc1 - gc0) * 4u;
+  if (lane == 0) mbar_expect_tx(bar, bytes * uint32_t(nrows));
+  __syncwarp();
+  const int dcol = gc0 - (b.x0 - Gm::RP);
+  for (int i = lane; i < nrows; i += 32) {
+    const int gy = reflect(r0 + i, H);
+    bulk_g2s(in + (idx0 + i) * Gm::PITCH + dcol, uin + size_t(gy) * W + gc0, bytes, bar);
+  }
+}
+
+template <int R, bool EDGE>
+__global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const StreamArgs a) {
+  using Gm = SGeo<R>;
+  extern __shared__ __align__(128) float smem[];
+  float* const in0 = smem;
+  float* const in1 = smem + Gm::IN_FLOATS;
+  float* const h0 = smem + 2 * Gm::IN_FLOATS;
+  float* const h1 = h0 + Gm::H_FLOATS;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(h1 + Gm::H_FLOATS);
+  __shared__ double s_red[kSCW];
+  __shared__ int s_nf[kSCW];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const int iter = (a.st.iter_base ? a.st.iter_base[0] : 0) + a.iter_off;
+  if (iter > a.max_iters) return;
+
+  if (warp == kSCW) {  // service warp
+    if (a.st.stop_iter && blockIdx.x == 0 && iter >= 2)
+      finalize_iteration_warp(a.st, a.pt, a.P, iter - 1, a.max_iters, a.rel_tol);
+    return;
+  }
+
+  const int H = a.H, W = a.W;
+  const size_t plane = size_t(H) * W;
+  const float* __restrict__ uin_all = ((iter - 1) & 1) ? a.buf1 : a.buf0;
+  float* __restrict__ uout_all = (iter & 1) ? a.buf1 : a.buf0;
+  const int64_t L0 = cta_start(blockIdx.x, a.pt.S, a.pt.G);
+  const int64_t L1 = cta_start(blockIdx.x + 1, a.pt.S, a.pt.G);
+  int64_t L = L0;
+
+  SBlock cur, nxt;
+  bool have = next_block(L, L0, L1, a, iter, cur);
+  if (have && warp == 0)
+    issue_rows<R>(cur, uin_all + cur.p * plane, in0, &bars[0], H, W, lane);
+
+  // thread roles for the vertical pass / update: column pair, 8-row group
+  const int c = 2 * lane;         // strip-local output column of the pair
+  const int j0 = warp * 8;        // block-local first row
+  uint32_t phase0 = 0, phase1 = 0;
+  int ib = 0;
+  double acc_r2 = 0.0;
+  float acc_nf = 0.0f;
+  int acc_p = have ? cur.p : -1;
+
+  while (have) {
+    const bool have_nxt = next_block(L, L0, L1, a, iter, nxt);
+    float* const in_cur = ib ? in1 : in0;
+    float* const in_nxt = ib ? in0 : in1;
+    float* const h_cur = ib ? h1 : h0;
+    float* const h_prev = ib ? h0 : h1;
+    uint64_t* const bar_cur = &bars[ib];
+    uint64_t* const bar_nxt = &bars[ib ^ 1];
+    const int gx = cur.x0 + c;
+    const bool col_ok = gx < W;
+    const float* __restrict__ uin = uin_all + cur.p * plane;
+
+    // ---- prefetch Phi / lambda for this thread's outputs into registers
+    float2 phv[8], lmv[8];
+    {
+      const float* __restrict__ ph = a.phi + cur.p * plane;
+      const float* __restrict__ lm = a.lam + (cur.p / a.C) * plane;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int y = cur.yb + j0 + j;
+        if (col_ok && j0 + j < cur.n) {
+          phv[j] = __ldg(reinterpret_cast<const float2*>(ph + size_t(y) * W + gx));
+          lmv[j] = __ldg(reinterpret_cast<const float2*>(lm + size_t(y) * W + gx));
+        } else {
+          phv[j] = make_float2(0.f, 0.f);
+          lmv[j] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+
+    // ---- wait for this block's input rows; mirror out-of-image columns
+    if (ib) {
+      mbar_wait(bar_cur, phase1);
+      phase1 ^= 1;
+    } else {
+      mbar_wait(bar_cur, phase0);
+      phase0 ^= 1;
+    }
+    const int new0 = cur.first ? 0 : R + 1;
+    const int nnew = cur.first ? cur.n + 2 * R : cur.n;
+    const int xbase = cur.x0 - Gm::RP;  // global column of staged column 0
+    if (xbase < 0 || xbase + Gm::PWD > W) {
+      for (int k = tid; k < nnew * Gm::PWD; k += kComputeThreads) {
+        const int i = k / Gm::PWD, ci = k - i * Gm::PWD;
+        const int g = xbase + ci;
+        if (g < 0 || g >= W) {
+          const int src = reflect(g, W) - xbase;
+          if (src >= 0 && src < Gm::PWD)
+            in_cur[(new0 + i) * Gm::PITCH + ci] = in_cur[(new0 + i) * Gm::PITCH + src];
+        }
+      }
+    }
+    compute_bar();
+
+    // ---- queue the next block's rows (+ carry of the R+1 overlap rows)
+    if (have_nxt) {
+      if (!nxt.first) {
+        // rows [nxt.yb - 1, nxt.yb + R) live in in_cur at idx (row - cur_base)
+        const int cur_base = cur.first ? cur.yb - R : cur.yb - 1;
+        const int s0 = (nxt.yb - 1) - cur_base;
+        const int nf4 = (R + 1) * (Gm::PWD / 4);
+        for (int k = tid; k < nf4; k += kComputeThreads) {
+          const int i = k / (Gm::PWD / 4), q = k - i * (Gm::PWD / 4);
+          reinterpret_cast<float4*>(in_nxt + i * Gm::PITCH)[q] =
+              reinterpret_cast<const float4*>(in_cur + (s0 + i) * Gm::PITCH)[q];
+        }
+      }
+      if (warp == 0)
+        issue_rows<R>(nxt, uin_all + nxt.p * plane, in_nxt, bar_nxt, H, W, lane);
+    }
+
+    // ---- H rows: carry the 2R overlap, blur the new rows
+    int hnew0, hn, in0row;
+    if (cur.first) {
+      hnew0 = 0;
+      hn = cur.n + 2 * R;
+      in0row = 0;
+    } else {
+      for (int k = tid; k < 2 * R * (kSTW / 4); k += kComputeThreads)
+        reinterpret_cast<float4*>(h_cur)[k] =
+            reinterpret_cast<const float4*>(h_prev + kSRB * kSTW)[k];
+      hnew0 = 2 * R;
+      hn = cur.n;
+      in0row = R + 1;
+    }
+    for (int item = tid; item < hn * (kSTW / 4); item += kComputeThreads) {
+      const int i = item >> 4, g = item & 15;
+      const float* row = in_cur + (in0row + i) * Gm::PITCH + 4 * g;
+      constexpr int NQ = (Gm::RP + R + 3) / 4 + 1;
+      float v[4 * NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 t = reinterpret_cast<const float4*>(row)[q];
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+      }
+      constexpr int OFF = Gm::RP - R;
+      float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+#pragma unroll
+      for (int k = 0; k <= 2 * R; ++k) {
+        const float wk = a.w[k];
+        o0 = fmaf(wk, v[OFF + k], o0);
+        o1 = fmaf(wk, v[OFF + k + 1], o1);
+        o2 = fmaf(wk, v[OFF + k + 2], o2);
+        o3 = fmaf(wk, v[OFF + k + 3], o3);
+      }
+      reinterpret_cast<float4*>(h_cur + (hnew0 + i) * kSTW)[g] = make_float4(o0, o1, o2, o3);
+    }
+    compute_bar();
+
+    // ---- vertical pass (FFMA2 over the column pair), divergence, update
+    if (j0 < cur.n) {
+      float2 G[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) G[j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 8 + 2 * R; ++k) {
+        const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * kSTW + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int t = k - j;
+          if (t >= 0 && t <= 2 * R) G[j] = ffma2(make_float2(a.w[t], a.w[t]), hv, G[j]);
+        }
+      }
+
+      // u rows y-1 .. y+8 at columns c-1 .. c+2 (staged column RP + c is aligned)
+      const int ubase = (cur.first ? R : 1) + j0 - 1;
+      float ul[10], ur[10];
+      float2 uc[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const float* row = in_cur + (ubase + i) * Gm::PITCH + Gm::RP + c;
+        uc[i] = *reinterpret_cast<const float2*>(row);
+        ul[i] = row[-1];
+        ur[i] = row[2];
+      }
+      const float sx0 = (gx == 0) ? 1.0f : 0.5f;           // column c   (c >= 0)
+      const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;   // column c+1
+      float2 cx[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i)
+        cx[i] = make_float2(sx0 * (uc[i].y - ul[i]), sx1 * (ur[i] - uc[i].x));
+      // south flux of the row above the first output row
+      float2 fs_up = make_float2(
+          sflux<EDGE>(uc[1].x - uc[0].x, 0.5f * (cx[0].x + cx[1].x), a.eps),
+          sflux<EDGE>(uc[1].y - uc[0].y, 0.5f * (cx[0].y + cx[1].y), a.eps));
+      float r2 = 0.f;
+      float* __restrict__ uout = uout_all + cur.p * plane;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int y = cur.yb + j0 + j;
+        const float sy = (y == 0 || y == H - 1) ? 1.0f : 0.5f;
+        // centred vertical differences at columns c-1, c, c+1, c+2
+        const float dl = sy * (ul[j + 2] - ul[j]);
+        const float d0 = sy * (uc[j + 2].x - uc[j].x);
+        const float d1 = sy * (uc[j + 2].y - uc[j].y);
+        const float dr = sy * (ur[j + 2] - ur[j]);
+        const float u0 = uc[j + 1].x, u1 = uc[j + 1].y;
+        const float fw = sflux<EDGE>(u0 - ul[j + 1], 0.5f * (dl + d0), a.eps);  // face c-1|c
+        const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);         // face c|c+1
+        const float fe = sflux<EDGE>(ur[j + 1] - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
+        const float2 fs_dn = make_float2(
+            sflux<EDGE>(uc[j + 2].x - u0, 0.5f * (cx[j + 1].x + cx[j + 2].x), a.eps),
+            sflux<EDGE>(uc[j + 2].y - u1, 0.5f * (cx[j + 1].y + cx[j + 2].y), a.eps));
+        const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
+        const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
+        fs_up = fs_dn;
+        const float r0 = fmaf(-lmv[j].x, G[j].x, div0) + phv[j].x;
+        const float r1 = fmaf(-lmv[j].y, G[j].y, div1) + phv[j].y;
+        const float n0 = fmaf(a.tau, r0, u0);
+        const float n1 = fmaf(a.tau, r1, u1);
+        if (col_ok && j0 + j < cur.n) {
+          *reinterpret_cast<float2*>(uout + size_t(y) * W + gx) = make_float2(n0, n1);
+          r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
+          acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff a non-finite update
+        }
+      }
+      acc_r2 += double(r2);
+    }
+
+    // ---- flush the plane partial when the plane changes / at the end
+    const bool flush = !have_nxt || nxt.p != acc_p;
+    if (flush) {
+      double s = warp_sum(acc_r2);
+      const int nfw = __any_sync(0xffffffffu, !(acc_nf == 0.0f));
+      if (lane == 0) {
+        s_red[warp] = s;
+        s_nf[warp] = nfw;
+      }
+      compute_bar();
+      if (tid == 0) {
+        double t = 0.0;
+        int f = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < kSCW; ++w2) {
+          t += s_red[w2];
+          f |= s_nf[w2];
+        }
+        const int k = int(blockIdx.x - cta_of(int64_t(acc_p) * a.pt.U, a.pt.S, a.pt.G));
+        const size_t slot = (size_t(iter & 1) * a.P + acc_p) * a.pt.nbmax + k;
+        a.pt.sum[slot] = t;
+        a.pt.flag[slot] = f;
+      }
+      acc_r2 = 0.0;
+      acc_nf = 0.0f;
+      acc_p = have_nxt ? nxt.p : -1;
+    }
+    cur = nxt;
+    have = have_nxt;
+    ib ^= 1;
+  }
+  pdl_launch_dependents();
+}
+
+// ------------------------------------------------------------------- host --
+using StreamFn = void (*)(const StreamArgs);
+
+template <int R, bool EDGE>
+static StreamFn stream_prepared(size_t* smem) {
+  static bool done = false;
+  *smem = SGeo<R>::SMEM;
+  if (!done) {
+    cudaFuncSetAttribute(stream_kernel<R, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(SGeo<R>::SMEM));
+    done = true;
+  }
+  return stream_kernel<R, EDGE>;
+}
+
+template <bool EDGE>
+static StreamFn stream_pick(int R, size_t* smem) {
+  switch (R) {
+    case 1: return stream_prepared<1, EDGE>(smem);
+    case 2: return stream_prepared<2, EDGE>(smem);
+    case 3: return stream_prepared<3, EDGE>(smem);
+    case 6: return stream_prepared<6, EDGE>(smem);
+    case 9: return stream_prepared<9, EDGE>(smem);
+    case 12: return stream_prepared<12, EDGE>(smem);
+    case 24: return stream_prepared<24, EDGE>(smem);
+    default: return nullptr;
+  }
+}
+
+}  // namespace pdz

@@ -25,7 +25,8 @@
 #include <mutex>
 #include <vector>
 
-#include "pdz_internal.cuh"
+#include "pdz_solver.cuh"
+#include "pdz_stream.cuh"
 
 namespace pdz {
 
@@ -33,29 +34,13 @@ constexpr int kTW = 32;           // tile width  (one warp of columns)
 constexpr int kTH = 64;           // tile height
 constexpr int kThreads = 256;     // 8 warps
 constexpr int kRowsPerWarp = kTH / (kThreads / 32);
-constexpr int kMaxFusedRadius = 48;
-constexpr int kMaxTaps = 2 * kMaxFusedRadius + 1;
-constexpr int kChunk = 16;        // sweeps per captured graph chunk
-
-struct StateView {
-  int32_t* stop_iter;   // [P] 0 = running, else the iteration it stopped at
-  int32_t* converged;   // [P]
-  int32_t* failed;      // [P] iteration that went non-finite, 0 = never
-  int32_t* iters;       // [P] iterations whose norm is recorded
-  double* prev_norm;    // [P]
-  double* norms;        // [max_iters][P]
-  int32_t* running;     // [1] planes still running after the latest finalize
-  int32_t* iter_base;   // [1] first iteration of the current graph chunk
-  int32_t* chunk_ctr;   // [1]
-};
 
 struct SweepArgs {
   float* buf0;
   float* buf1;
   const float* phi;
   const float* lam;
-  double* partials;      // [2][P][nblk]
-  int32_t* nf_flags;     // [2][P][nblk]
+  Partials pt;           // [2][P][nblk] (tiles = nblk)
   StateView st;          // st.stop_iter == nullptr: single step, no stop rule
   int32_t H, W, P, C, R;
   int32_t tiles_x, nblk;
@@ -74,49 +59,6 @@ __device__ __forceinline__ float face_flux(float jump, float along, float eps) {
   if (!EDGE) return jump;
   const float g = sqrtf(fmaf(jump, jump, along * along));
   return __fdiv_rn(jump, g + eps);
-}
-
-// Reduce iteration `it`'s partials for every still-running plane and apply
-// the stop rule.  Executed by one whole block.
-__device__ void finalize_iteration(const SweepArgs& a, int it) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  for (int p = warp; p < a.P; p += nwarps) {
-    if (a.st.stop_iter[p] != 0) continue;
-    const size_t base = (size_t(it & 1) * a.P + p) * a.nblk;
-    double s = 0.0;
-    int nf = 0;
-    for (int b = lane; b < a.nblk; b += 32) {
-      s += a.partials[base + b];
-      nf |= a.nf_flags[base + b];
-    }
-    s = warp_sum(s);
-    nf = __any_sync(0xffffffffu, nf);
-    if (lane == 0) {
-      if (nf) {
-        a.st.failed[p] = it;
-        a.st.stop_iter[p] = it;
-      } else {
-        const double norm = sqrt(s);
-        a.st.norms[size_t(it - 1) * a.P + p] = norm;
-        a.st.iters[p] = it;
-        const double prev = a.st.prev_norm[p];
-        if (it >= 2 && fabs(norm - prev) / fmax(prev, 1e-30) <= a.rel_tol) {
-          a.st.converged[p] = 1;
-          a.st.stop_iter[p] = it;
-        } else if (it >= a.max_iters) {
-          a.st.stop_iter[p] = it;
-        }
-        a.st.prev_norm[p] = norm;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int p = 0; p < a.P; ++p) n += (a.st.stop_iter[p] == 0);
-    a.st.running[0] = n;
-  }
 }
 
 // ------------------------------------------------------------------------
@@ -143,8 +85,9 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
   const int iter = (a.st.iter_base ? a.st.iter_base[0] : 0) + a.iter_off;
   if (iter > a.max_iters) return;
   if (a.st.stop_iter) {
-    if (iter >= 2 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-      finalize_iteration(a, iter - 1);
+    if (iter >= 2 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+        threadIdx.x < 32)
+      finalize_iteration_warp(a.st, a.pt, a.P, iter - 1, a.max_iters, a.rel_tol);
     const int s = a.st.stop_iter[p];
     if (s != 0 && s < iter - 1) return;  // stopped at <= iter-2: frozen
   }
@@ -288,16 +231,17 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
       s += s_red[w];
       f |= s_nf[w];
     }
-    const size_t slot = (size_t(iter & 1) * a.P + p) * a.nblk + blk;
-    a.partials[slot] = s;
-    a.nf_flags[slot] = f;
+    const size_t slot = (size_t(iter & 1) * a.P + p) * a.pt.nbmax + blk;
+    a.pt.sum[slot] = s;
+    a.pt.flag[slot] = f;
   }
   pdl_launch_dependents();
 }
 
-__global__ void finalize_kernel(const SweepArgs a, int it) {
+__global__ void finalize_kernel(StateView st, Partials pt, int P, int it, int max_iters,
+                                double rel_tol) {
   pdl_wait();
-  finalize_iteration(a, it);
+  if (threadIdx.x < 32) finalize_iteration_warp(st, pt, P, it, max_iters, rel_tol);
 }
 
 // Chunk prologue: iter_base = chunk * kChunk + 1.
@@ -325,23 +269,19 @@ __global__ void init_state_kernel(StateView st, int P) {
   }
 }
 
-// Single fixed_point_step: norms[p] = sqrt(sum of iteration-1 partials).
-__global__ void step_norm_kernel(const SweepArgs a, double* norms, int32_t* nonfinite) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int p = warp; p < a.P; p += blockDim.x >> 5) {
-    const size_t base = (size_t(1) * a.P + p) * a.nblk;
+// Single fixed_point_step: norms[p] = sqrt(sum of the iteration-1 partials).
+__global__ void step_norm_kernel(Partials pt, int P, double* norms, int32_t* nonfinite) {
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const size_t base = (size_t(1) * P + p) * pt.nbmax;
+    const int n = partial_count(pt, p);
     double s = 0.0;
     int nf = 0;
-    for (int b = lane; b < a.nblk; b += 32) {
-      s += a.partials[base + b];
-      nf |= a.nf_flags[base + b];
+    for (int b = 0; b < n; ++b) {
+      s += pt.sum[base + b];
+      nf |= pt.flag[base + b];
     }
-    s = warp_sum(s);
-    nf = __any_sync(0xffffffffu, nf);
-    if (lane == 0) {
-      norms[p] = sqrt(s);
-      if (nonfinite) nonfinite[p] = nf;
-    }
+    norms[p] = sqrt(s);
+    if (nonfinite) nonfinite[p] = nf;
   }
 }
 
@@ -350,14 +290,16 @@ __global__ void step_norm_kernel(const SweepArgs a, double* norms, int32_t* nonf
 
 using SweepFn = void (*)(const SweepArgs);
 
+static size_t tile_smem(int R) {
+  return size_t(((kTH + 2 * R) * (kTW + 2 * R + 1) + 3 + (kTH + 2 * R) * kTW)) * 4;
+}
+
 template <int RT, bool EDGE>
 static SweepFn prepared() {
   static bool done = false;
   if (!done) {
-    const int R = RT >= 0 ? RT : kMaxFusedRadius;
-    const size_t smem = size_t(((kTH + 2 * R) * (kTW + 2 * R + 1) + 3 + (kTH + 2 * R) * kTW)) * 4;
     cudaFuncSetAttribute(sweep_kernel<RT, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+                         int(tile_smem(RT >= 0 ? RT : kMaxFusedRadius)));
     done = true;
   }
   return sweep_kernel<RT, EDGE>;
@@ -377,16 +319,22 @@ static SweepFn pick_kernel(int R) {
   }
 }
 
-static size_t sweep_smem(int R) {
-  return size_t(((kTH + 2 * R) * (kTW + 2 * R + 1) + 3 + (kTH + 2 * R) * kTW)) * 4;
-}
-
-struct Geometry {
-  int R;        // fused-kernel radius (>= 1)
-  int tiles_x, tiles_y, nblk;
+// How one sweep is launched: the streaming kernel (width % 4 == 0 and a
+// compiled radius) or the tiled fallback.
+struct Plan {
+  bool stream = false;
+  int R = 1;
+  int tiles_x = 0, tiles_y = 0, nblk = 0;  // tiled
+  int G = 0, nstrips = 0;                   // streaming
+  int64_t S = 0, U = 0;
+  int nbmax = 0;                            // partial slots per plane
+  size_t smem = 0;
+  void* fn = nullptr;
 };
 
-static int32_t check_params(const pdz_solve_params* p, Geometry* g) {
+static int g_force_tiled = -1;  // PDZ_FORCE_TILED=1 -> always the tiled kernel
+
+static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
   PDZ_REQUIRE(p != nullptr, "params is NULL");
   PDZ_REQUIRE(p->height >= 2 && p->width >= 2, "field must be at least 2x2, got (%d, %d)",
               p->height, p->width);
@@ -401,78 +349,160 @@ static int32_t check_params(const pdz_solve_params* p, Geometry* g) {
   PDZ_REQUIRE(p->epsilon > 0.0, "epsilon must be > 0");
   PDZ_REQUIRE(p->max_iters >= 1, "max_iters must be >= 1");
   PDZ_REQUIRE(std::isfinite(p->tau), "tau must be finite");
-  if (g) {
-    g->R = std::max(1, p->kernel_size / 2);
-    g->tiles_x = (p->width + kTW - 1) / kTW;
-    g->tiles_y = (p->height + kTH - 1) / kTH;
-    g->nblk = g->tiles_x * g->tiles_y;
+  if (!pl) return PDZ_OK;
+  if (g_force_tiled < 0) {
+    const char* e = getenv("PDZ_FORCE_TILED");
+    g_force_tiled = (e && e[0] == '1') ? 1 : 0;
+  }
+  Plan& P = *pl;
+  P.R = std::max(1, p->kernel_size / 2);
+  const bool edge = p->edge_preserving != 0;
+  size_t smem = 0;
+  StreamFn sfn = nullptr;
+  if (!g_force_tiled && p->width % 4 == 0)
+    sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
+  if (sfn) {
+    P.stream = true;
+    P.fn = reinterpret_cast<void*>(sfn);
+    P.smem = smem;
+    P.nstrips = (p->width + kSTW - 1) / kSTW;
+    P.U = int64_t(P.nstrips) * p->height;
+    P.S = P.U * p->planes;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
+    occ = std::max(1, occ);
+    const int64_t gmax = int64_t(num_sms()) * occ;
+    P.G = int(std::max<int64_t>(1, std::min<int64_t>(gmax, P.S / 16)));
+    int nb = 1;
+    for (int q = 0; q < p->planes; ++q) {
+      const int64_t lo = cta_of(int64_t(q) * P.U, P.S, P.G);
+      const int64_t hi = cta_of(int64_t(q + 1) * P.U - 1, P.S, P.G);
+      nb = std::max<int>(nb, int(hi - lo + 1));
+    }
+    P.nbmax = nb;
+  } else {
+    P.stream = false;
+    P.fn = reinterpret_cast<void*>(edge ? pick_kernel<true>(P.R) : pick_kernel<false>(P.R));
+    P.smem = tile_smem(P.R);
+    P.tiles_x = (p->width + kTW - 1) / kTW;
+    P.tiles_y = (p->height + kTH - 1) / kTH;
+    P.nblk = P.tiles_x * P.tiles_y;
+    P.nbmax = P.nblk;
   }
   return PDZ_OK;
 }
 
-static int32_t fill_args(const pdz_solve_params* p, const Geometry& g, SweepArgs* a) {
-  memset(a, 0, sizeof(*a));
+// Kernel arguments for either kernel (the launcher passes the right one).
+struct LaunchArgs {
+  SweepArgs tile;
+  StreamArgs stream;
+};
+
+static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0, float* buf1,
+                         const float* phi, const float* lam, double* psum, int32_t* pflag,
+                         const StateView& st, LaunchArgs* la) {
+  memset(la, 0, sizeof(*la));
   double taps[kMaxTaps];
-  int32_t st = gaussian_taps_host(p->sigma, p->kernel_size, taps);
-  if (st != PDZ_OK) return st;
+  int32_t rc = gaussian_taps_host(p->sigma, p->kernel_size, taps);
+  if (rc != PDZ_OK) return rc;
+  float w[kMaxTaps] = {0.f};
   const int K = p->kernel_size;
   if (K == 1) {  // identity smoothing expressed as taps (0, 1, 0), R = 1
-    a->w[0] = 0.f;
-    a->w[1] = float(taps[0]);
-    a->w[2] = 0.f;
+    w[1] = float(taps[0]);
   } else {
-    for (int i = 0; i < K; ++i) a->w[i] = float(taps[i]);
+    for (int i = 0; i < K; ++i) w[i] = float(taps[i]);
   }
-  a->H = p->height;
-  a->W = p->width;
-  a->P = p->planes;
-  a->C = p->channels;
-  a->R = g.R;
-  a->tiles_x = g.tiles_x;
-  a->nblk = g.nblk;
-  a->max_iters = p->max_iters;
-  a->eps = float(p->epsilon);
-  a->tau = float(p->tau);
-  a->rel_tol = p->rel_tol;
+  Partials pt;
+  pt.sum = psum;
+  pt.flag = pflag;
+  pt.nbmax = pl.nbmax;
+  pt.tiles = pl.stream ? 0 : pl.nblk;
+  pt.S = pl.S;
+  pt.U = pl.U;
+  pt.G = pl.G;
+  SweepArgs& a = la->tile;
+  a.buf0 = buf0;
+  a.buf1 = buf1;
+  a.phi = phi;
+  a.lam = lam;
+  a.pt = pt;
+  a.st = st;
+  a.H = p->height;
+  a.W = p->width;
+  a.P = p->planes;
+  a.C = p->channels;
+  a.R = pl.R;
+  a.tiles_x = pl.tiles_x;
+  a.nblk = pl.nblk;
+  a.max_iters = p->max_iters;
+  a.eps = float(p->epsilon);
+  a.tau = float(p->tau);
+  a.rel_tol = p->rel_tol;
+  memcpy(a.w, w, sizeof(w));
+  StreamArgs& b = la->stream;
+  b.buf0 = buf0;
+  b.buf1 = buf1;
+  b.phi = phi;
+  b.lam = lam;
+  b.pt = pt;
+  b.st = st;
+  b.H = p->height;
+  b.W = p->width;
+  b.P = p->planes;
+  b.C = p->channels;
+  b.nstrips = pl.nstrips;
+  b.max_iters = p->max_iters;
+  b.eps = float(p->epsilon);
+  b.tau = float(p->tau);
+  b.rel_tol = p->rel_tol;
+  memcpy(b.w, w, sizeof(w));
   return PDZ_OK;
 }
 
-static int32_t launch_sweep(const SweepArgs& a, const pdz_solve_params* p, const Geometry& g,
-                            cudaStream_t s, bool pdl) {
-  SweepFn fn = p->edge_preserving ? pick_kernel<true>(g.R) : pick_kernel<false>(g.R);
+static int32_t launch_sweep(LaunchArgs la, const pdz_solve_params* p, const Plan& pl,
+                            int iter_off, cudaStream_t s, bool pdl) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.tiles_x, g.tiles_y, p->planes);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = sweep_smem(g.R);
   cfg.stream = s;
+  cfg.dynamicSmemBytes = pl.smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  PDZ_CUDA(cudaLaunchKernelEx(&cfg, fn, a), "sweep launch");
+  if (pl.stream) {
+    la.stream.iter_off = iter_off;
+    cfg.gridDim = dim3(pl.G);
+    cfg.blockDim = dim3(kSThreads);
+    PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<StreamFn>(pl.fn), la.stream),
+             "stream sweep launch");
+  } else {
+    la.tile.iter_off = iter_off;
+    cfg.gridDim = dim3(pl.tiles_x, pl.tiles_y, p->planes);
+    cfg.blockDim = dim3(kThreads);
+    PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<SweepFn>(pl.fn), la.tile),
+             "tiled sweep launch");
+  }
   return PDZ_OK;
 }
 
 struct SolveLayout {
   float* buf0;
   float* buf1;
-  double* partials;
-  int32_t* flags;
+  double* psum;
+  int32_t* pflag;
   StateView st;
   size_t bytes;
 };
 
-static SolveLayout carve_solve(const pdz_solve_params* p, const Geometry& g, void* ws,
-                               size_t cap) {
+static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* ws, size_t cap) {
   Carver c(ws, cap);
   SolveLayout L = {};
   const size_t plane = size_t(p->height) * p->width;
   const size_t P = p->planes;
   L.buf0 = c.take<float>(P * plane);
   L.buf1 = c.take<float>(P * plane);
-  L.partials = c.take<double>(2 * P * g.nblk);
-  L.flags = c.take<int32_t>(2 * P * g.nblk);
+  L.psum = c.take<double>(2 * P * pl.nbmax);
+  L.pflag = c.take<int32_t>(2 * P * pl.nbmax);
   L.st.stop_iter = c.take<int32_t>(P);
   L.st.converged = c.take<int32_t>(P);
   L.st.failed = c.take<int32_t>(P);
@@ -486,7 +516,7 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Geometry& g, voi
   return L;
 }
 
-// Graph cache: one instantiated chunk graph per (args, stream) signature.
+// Graph cache: one instantiated chunk graph per (args, params, stream).
 struct GraphKey {
   std::vector<unsigned char> bytes;
   bool operator<(const GraphKey& o) const { return bytes < o.bytes; }
@@ -494,13 +524,13 @@ struct GraphKey {
 static std::mutex g_graph_mu;
 static std::map<GraphKey, cudaGraphExec_t> g_graphs;
 
-static int32_t chunk_graph(const SweepArgs& base, const pdz_solve_params* p, const Geometry& g,
+static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, const Plan& pl,
                            cudaStream_t s, cudaGraphExec_t* out) {
   GraphKey key;
-  key.bytes.resize(sizeof(SweepArgs) + sizeof(pdz_solve_params) + sizeof(void*));
-  memcpy(key.bytes.data(), &base, sizeof(SweepArgs));
-  memcpy(key.bytes.data() + sizeof(SweepArgs), p, sizeof(pdz_solve_params));
-  memcpy(key.bytes.data() + sizeof(SweepArgs) + sizeof(pdz_solve_params), &s, sizeof(void*));
+  key.bytes.resize(sizeof(LaunchArgs) + sizeof(pdz_solve_params) + sizeof(void*));
+  memcpy(key.bytes.data(), &la, sizeof(LaunchArgs));
+  memcpy(key.bytes.data() + sizeof(LaunchArgs), p, sizeof(pdz_solve_params));
+  memcpy(key.bytes.data() + sizeof(LaunchArgs) + sizeof(pdz_solve_params), &s, sizeof(void*));
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     auto it = g_graphs.find(key);
@@ -513,13 +543,9 @@ static int32_t chunk_graph(const SweepArgs& base, const pdz_solve_params* p, con
   PDZ_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
   cudaGraph_t graph;
   PDZ_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
-  chunk_base_kernel<<<1, 1, 0, cap>>>(base.st);
+  chunk_base_kernel<<<1, 1, 0, cap>>>(la.tile.st);
   int32_t rc = PDZ_OK;
-  for (int i = 0; i < kChunk && rc == PDZ_OK; ++i) {
-    SweepArgs a = base;
-    a.iter_off = i;
-    rc = launch_sweep(a, p, g, cap, true);
-  }
+  for (int i = 0; i < kChunk && rc == PDZ_OK; ++i) rc = launch_sweep(la, p, pl, i, cap, true);
   cudaError_t e = cudaStreamEndCapture(cap, &graph);
   cudaStreamDestroy(cap);
   if (rc != PDZ_OK) return rc;
@@ -539,23 +565,15 @@ static int32_t chunk_graph(const SweepArgs& base, const pdz_solve_params* p, con
   return PDZ_OK;
 }
 
-// Queue init + all sweeps (graph chunks) on the stream.  If `poll` is set the
-// host watches the device `running` counter (lagged by one chunk) and stops
-// queueing once every plane has stopped.  Returns the last iteration queued.
-static int32_t queue_solve(const pdz_solve_params* p, const Geometry& g, const SolveLayout& L,
+// Queue init + all sweeps (graph chunks) on the stream.  With `poll` the host
+// watches the device `running` counter (lagged by one chunk) and stops
+// queueing once every plane has stopped.
+static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
                            const float* phi, const float* lam, cudaStream_t s, bool poll,
                            int* last_iter) {
-  SweepArgs a;
-  int32_t rc = fill_args(p, g, &a);
+  LaunchArgs la;
+  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, phi, lam, L.psum, L.pflag, L.st, &la);
   if (rc != PDZ_OK) return rc;
-  a.buf0 = L.buf0;
-  a.buf1 = L.buf1;
-  a.phi = phi;
-  a.lam = lam;
-  a.partials = L.partials;
-  a.nf_flags = L.flags;
-  a.st = L.st;
-
   const size_t plane_bytes = size_t(p->height) * p->width * sizeof(float);
   PDZ_CUDA(cudaMemcpyAsync(L.buf0, phi, plane_bytes * p->planes, cudaMemcpyDeviceToDevice, s),
            "u0 = Phi");
@@ -563,7 +581,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Geometry& g, const S
   PDZ_CHECK_LAUNCH("init state");
 
   cudaGraphExec_t exec;
-  rc = chunk_graph(a, p, g, s, &exec);
+  rc = chunk_graph(la, p, pl, s, &exec);
   if (rc != PDZ_OK) return rc;
 
   const int n_chunks = (p->max_iters + kChunk - 1) / kChunk;
@@ -591,16 +609,19 @@ static int32_t queue_solve(const pdz_solve_params* p, const Geometry& g, const S
       PDZ_CUDA(cudaEventRecord(events[slot], s), "poll record");
     }
   }
+  Partials pt = la.tile.pt;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(32);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  PDZ_CUDA(cudaLaunchKernelEx(&cfg, finalize_kernel, a, launched), "finalize launch");
+  PDZ_CUDA(cudaLaunchKernelEx(&cfg, finalize_kernel, L.st, pt, int(p->planes), launched,
+                              int(p->max_iters), p->rel_tol),
+           "finalize launch");
   *last_iter = launched;
   return PDZ_OK;
 }
@@ -612,11 +633,11 @@ using namespace pdz;
 extern "C" {
 
 size_t pdz_step_workspace_bytes(const pdz_solve_params* params) {
-  Geometry g;
-  if (check_params(params, &g) != PDZ_OK) return 0;
+  Plan pl;
+  if (check_params(params, &pl) != PDZ_OK) return 0;
   Carver c(nullptr, 0);
-  c.take<double>(2 * size_t(params->planes) * g.nblk);
-  c.take<int32_t>(2 * size_t(params->planes) * g.nblk);
+  c.take<double>(2 * size_t(params->planes) * pl.nbmax);
+  c.take<int32_t>(2 * size_t(params->planes) * pl.nbmax);
   return Carver::round(c.off);
 }
 
@@ -624,41 +645,37 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
                              const float* phi, const float* lambda_map, double* norms,
                              int32_t* nonfinite, void* workspace, size_t workspace_bytes,
                              void* stream) {
-  Geometry g;
-  int32_t rc = check_params(params, &g);
+  Plan pl;
+  int32_t rc = check_params(params, &pl);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(u && u_out && phi && lambda_map && norms, "NULL array argument");
   PDZ_REQUIRE(u != u_out, "u_out must not alias u");
   Carver c(workspace, workspace_bytes);
-  double* partials = c.take<double>(2 * size_t(params->planes) * g.nblk);
-  int32_t* flags = c.take<int32_t>(2 * size_t(params->planes) * g.nblk);
+  double* psum = c.take<double>(2 * size_t(params->planes) * pl.nbmax);
+  int32_t* pflag = c.take<int32_t>(2 * size_t(params->planes) * pl.nbmax);
   if (!c.ok) {
     set_error("workspace too small: need %zu bytes, got %zu", c.off, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
-  SweepArgs a;
-  rc = fill_args(params, g, &a);
+  pdz_solve_params one = *params;
+  one.max_iters = 1;
+  LaunchArgs la;
+  StateView none = {};
+  rc = fill_args(&one, pl, const_cast<float*>(u), u_out, phi, lambda_map, psum, pflag, none,
+                 &la);  // iteration 1 reads buf0 (= u), writes buf1 (= u_out)
   if (rc != PDZ_OK) return rc;
-  a.buf0 = const_cast<float*>(u);  // iteration 1 reads buf0, writes buf1
-  a.buf1 = u_out;
-  a.phi = phi;
-  a.lam = lambda_map;
-  a.partials = partials;
-  a.nf_flags = flags;
-  a.iter_off = 1;
-  a.max_iters = 1;
   cudaStream_t s = as_stream(stream);
-  rc = launch_sweep(a, params, g, s, false);
+  rc = launch_sweep(la, &one, pl, 1, s, false);
   if (rc != PDZ_OK) return rc;
-  step_norm_kernel<<<1, 256, 0, s>>>(a, norms, nonfinite);
+  step_norm_kernel<<<1, 256, 0, s>>>(la.tile.pt, params->planes, norms, nonfinite);
   PDZ_CHECK_LAUNCH("step norm");
   return PDZ_OK;
 }
 
 size_t pdz_solve_workspace_bytes(const pdz_solve_params* params) {
-  Geometry g;
-  if (check_params(params, &g) != PDZ_OK) return 0;
-  return Carver::round(carve_solve(params, g, nullptr, 0).bytes);
+  Plan pl;
+  if (check_params(params, &pl) != PDZ_OK) return 0;
+  return Carver::round(carve_solve(params, pl, nullptr, 0).bytes);
 }
 
 int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
@@ -666,24 +683,23 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
                               int32_t* iterations_host, int32_t* converged_host,
                               int32_t* failed_host, void* workspace, size_t workspace_bytes,
                               void* stream) {
-  Geometry g;
-  int32_t rc = check_params(params, &g);
+  Plan pl;
+  int32_t rc = check_params(params, &pl);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(phi && lambda_map && u_out, "NULL array argument");
   PDZ_REQUIRE(norms_host && iterations_host && converged_host && failed_host,
               "NULL host output");
-  SolveLayout L = carve_solve(params, g, workspace, workspace_bytes);
+  SolveLayout L = carve_solve(params, pl, workspace, workspace_bytes);
   if (workspace == nullptr || L.bytes > workspace_bytes) {
     set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
   cudaStream_t s = as_stream(stream);
   int last = 0;
-  rc = queue_solve(params, g, L, phi, lambda_map, s, true, &last);
+  rc = queue_solve(params, pl, L, phi, lambda_map, s, true, &last);
   if (rc != PDZ_OK) return rc;
   const int P = params->planes;
   PDZ_CUDA(cudaStreamSynchronize(s), "solve sync");
-  std::vector<int32_t> stop(P);
   PDZ_CUDA(cudaMemcpy(iterations_host, L.st.iters, P * 4, cudaMemcpyDeviceToHost), "D2H iters");
   PDZ_CUDA(cudaMemcpy(converged_host, L.st.converged, P * 4, cudaMemcpyDeviceToHost), "D2H conv");
   PDZ_CUDA(cudaMemcpy(failed_host, L.st.failed, P * 4, cudaMemcpyDeviceToHost), "D2H failed");
@@ -692,13 +708,13 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
            "D2H norms");
   const size_t plane = size_t(params->height) * params->width;
   int worst = -1;
-  for (int p = 0; p < P; ++p) {
-    const int it = iterations_host[p];
+  for (int q = 0; q < P; ++q) {
+    const int it = iterations_host[q];
     const float* src = (it & 1) ? L.buf1 : L.buf0;
-    PDZ_CUDA(cudaMemcpyAsync(u_out + p * plane, src + p * plane, plane * 4,
+    PDZ_CUDA(cudaMemcpyAsync(u_out + q * plane, src + q * plane, plane * 4,
                              cudaMemcpyDeviceToDevice, s),
              "final iterate");
-    if (failed_host[p] != 0 && worst < 0) worst = p;
+    if (failed_host[q] != 0 && worst < 0) worst = q;
   }
   PDZ_CUDA(cudaStreamSynchronize(s), "solve sync");
   if (worst >= 0) {
@@ -712,35 +728,40 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
 int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float* phi,
                                      const float* lambda_map, void* workspace,
                                      size_t workspace_bytes, void* stream) {
-  Geometry g;
-  int32_t rc = check_params(params, &g);
+  Plan pl;
+  int32_t rc = check_params(params, &pl);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(phi && lambda_map, "NULL array argument");
   pdz_solve_params fixed = *params;
   fixed.rel_tol = -1.0;  // never stops early
-  SolveLayout L = carve_solve(&fixed, g, workspace, workspace_bytes);
+  SolveLayout L = carve_solve(&fixed, pl, workspace, workspace_bytes);
   if (workspace == nullptr || L.bytes > workspace_bytes) {
     set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
   int last = 0;
-  return queue_solve(&fixed, g, L, phi, lambda_map, as_stream(stream), false, &last);
+  return queue_solve(&fixed, pl, L, phi, lambda_map, as_stream(stream), false, &last);
 }
 
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {
-  Geometry g;
-  if (check_params(params, &g) != PDZ_OK) return -1;
+  if (check_params(params, nullptr) != PDZ_OK) return -1;
   const int64_t chunks = (params->max_iters + kChunk - 1) / kChunk;
   return 2 + chunks * (1 + kChunk);  // init + chunk prologues + sweeps + finalize
 }
 
 const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* workspace,
                                     int32_t plane, int32_t iterations) {
-  Geometry g;
-  if (check_params(params, &g) != PDZ_OK || workspace == nullptr) return nullptr;
-  SolveLayout L = carve_solve(params, g, const_cast<void*>(workspace), ~size_t(0) >> 1);
+  Plan pl;
+  if (check_params(params, &pl) != PDZ_OK || workspace == nullptr) return nullptr;
+  SolveLayout L = carve_solve(params, pl, const_cast<void*>(workspace), ~size_t(0) >> 1);
   const size_t n = size_t(params->height) * params->width;
   return ((iterations & 1) ? L.buf1 : L.buf0) + plane * n;
+}
+
+int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params) {
+  Plan pl;
+  if (check_params(params, &pl) != PDZ_OK) return -1;
+  return pl.stream ? 2 : 1;
 }
 
 }  // extern "C"
