@@ -34,8 +34,8 @@
 namespace pdz {
 
 constexpr int kSTW = 64;                   // strip width (output columns)
-constexpr int kSRB = 64;                   // output rows per block
-constexpr int kSCW = 8;                    // compute warps
+constexpr int kSRB = 32;                   // output rows per block (4 warps x 8)
+constexpr int kSCW = 4;                    // compute warps
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
 
@@ -43,7 +43,7 @@ template <int R>
 struct SGeo {
   static constexpr int RP = (R + 3) & ~3;        // column halo rounded to float4
   static constexpr int PWD = kSTW + 2 * RP;      // staged floats per row
-  static constexpr int PITCH = (PWD + 31) & ~31;  // 128-byte aligned smem rows
+  static constexpr int PITCH = PWD;              // 16-byte aligned smem rows
   static constexpr int ROWS = kSRB + 2 * R;      // staged input rows / H rows
   static constexpr int IN_FLOATS = ROWS * PITCH;
   static constexpr int H_FLOATS = ROWS * kSTW;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void issue_rows(const SBlock& b, const float* __restr
 }
 
 template <int R, bool EDGE>
-__global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const StreamArgs a) {
+__global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a) {
   using Gm = SGeo<R>;
   extern __shared__ __align__(128) float smem[];
   float* const in0 = smem;
@@ -359,48 +359,47 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const StreamArgs a
         }
       }
 
-      // u rows y-1 .. y+8 at columns c-1 .. c+2 (staged column RP + c is aligned)
-      const int ubase = (cur.first ? R : 1) + j0 - 1;
-      float ul[10], ur[10];
-      float2 uc[10];
-#pragma unroll
-      for (int i = 0; i < 10; ++i) {
-        const float* row = in_cur + (ubase + i) * Gm::PITCH + Gm::RP + c;
-        uc[i] = *reinterpret_cast<const float2*>(row);
-        ul[i] = row[-1];
-        ur[i] = row[2];
-      }
+      // rolling window of u rows (A = y-1, B = y, C = y+1) at columns c-1 .. c+2
+      // (staged column RP + c is 8-byte aligned)
+      const float* urow = in_cur + ((cur.first ? R : 1) + j0 - 1) * Gm::PITCH + Gm::RP + c;
       const float sx0 = (gx == 0) ? 1.0f : 0.5f;           // column c   (c >= 0)
       const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;   // column c+1
-      float2 cx[10];
-#pragma unroll
-      for (int i = 0; i < 10; ++i)
-        cx[i] = make_float2(sx0 * (uc[i].y - ul[i]), sx1 * (ur[i] - uc[i].x));
+      float lA = urow[-1], rA = urow[2];
+      float2 cA = *reinterpret_cast<const float2*>(urow);
+      urow += Gm::PITCH;
+      float lB = urow[-1], rB = urow[2];
+      float2 cB = *reinterpret_cast<const float2*>(urow);
+      float2 xA = make_float2(sx0 * (cA.y - lA), sx1 * (rA - cA.x));
+      float2 xB = make_float2(sx0 * (cB.y - lB), sx1 * (rB - cB.x));
       // south flux of the row above the first output row
-      float2 fs_up = make_float2(
-          sflux<EDGE>(uc[1].x - uc[0].x, 0.5f * (cx[0].x + cx[1].x), a.eps),
-          sflux<EDGE>(uc[1].y - uc[0].y, 0.5f * (cx[0].y + cx[1].y), a.eps));
+      float2 fs_up = make_float2(sflux<EDGE>(cB.x - cA.x, 0.5f * (xA.x + xB.x), a.eps),
+                                 sflux<EDGE>(cB.y - cA.y, 0.5f * (xA.y + xB.y), a.eps));
       float r2 = 0.f;
       float* __restrict__ uout = uout_all + cur.p * plane;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
+        urow += Gm::PITCH;
+        const float lC = urow[-1], rC = urow[2];
+        const float2 cC = *reinterpret_cast<const float2*>(urow);
+        const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
         const int y = cur.yb + j0 + j;
         const float sy = (y == 0 || y == H - 1) ? 1.0f : 0.5f;
         // centred vertical differences at columns c-1, c, c+1, c+2
-        const float dl = sy * (ul[j + 2] - ul[j]);
-        const float d0 = sy * (uc[j + 2].x - uc[j].x);
-        const float d1 = sy * (uc[j + 2].y - uc[j].y);
-        const float dr = sy * (ur[j + 2] - ur[j]);
-        const float u0 = uc[j + 1].x, u1 = uc[j + 1].y;
-        const float fw = sflux<EDGE>(u0 - ul[j + 1], 0.5f * (dl + d0), a.eps);  // face c-1|c
-        const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);         // face c|c+1
-        const float fe = sflux<EDGE>(ur[j + 1] - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
-        const float2 fs_dn = make_float2(
-            sflux<EDGE>(uc[j + 2].x - u0, 0.5f * (cx[j + 1].x + cx[j + 2].x), a.eps),
-            sflux<EDGE>(uc[j + 2].y - u1, 0.5f * (cx[j + 1].y + cx[j + 2].y), a.eps));
+        const float dl = sy * (lC - lA);
+        const float d0 = sy * (cC.x - cA.x);
+        const float d1 = sy * (cC.y - cA.y);
+        const float dr = sy * (rC - rA);
+        const float u0 = cB.x, u1 = cB.y;
+        const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
+        const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
+        const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
+        const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
+                                         sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
         const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
         const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
         fs_up = fs_dn;
+        lA = lB; rA = rB; cA = cB; xA = xB;
+        lB = lC; rB = rC; cB = cC; xB = xC;
         const float r0 = fmaf(-lmv[j].x, G[j].x, div0) + phv[j].x;
         const float r1 = fmaf(-lmv[j].y, G[j].y, div1) + phv[j].y;
         const float n0 = fmaf(a.tau, r0, u0);
