@@ -135,13 +135,14 @@ struct SBlock {
 };
 
 // Next block of this CTA's range; skips planes frozen at <= iter-2.
-__device__ __forceinline__ bool next_block(int64_t& L, int64_t L0, int64_t L1,
-                                           const StreamArgs& a, int iter, SBlock& b) {
+// (32-bit arithmetic: the host only selects this kernel when S < 2^31.)
+__device__ __forceinline__ bool next_block(int& L, int L0, int L1, const StreamArgs& a,
+                                           int iter, SBlock& b) {
   while (L < L1) {
-    const int64_t u = L / a.H;
-    const int y = int(L - u * a.H);
-    const int64_t seg_end = min(L1, (u + 1) * int64_t(a.H));
-    const int p = int(u / a.nstrips);
+    const int u = L / a.H;
+    const int y = L - u * a.H;
+    const int seg_end = min(L1, (u + 1) * a.H);
+    const int p = u / a.nstrips;
     if (a.st.stop_iter) {
       const int s = a.st.stop_iter[p];
       if (s != 0 && s < iter - 1) {
@@ -150,9 +151,9 @@ __device__ __forceinline__ bool next_block(int64_t& L, int64_t L0, int64_t L1,
       }
     }
     b.p = p;
-    b.x0 = int(u - int64_t(p) * a.nstrips) * kSTW;
+    b.x0 = (u - p * a.nstrips) * kSTW;
     b.yb = y;
-    b.n = int(seg_end - L < kSRB ? seg_end - L : int64_t(kSRB));
+    b.n = min(kSRB, seg_end - L);
     b.first = (L == L0) || (y == 0);
     L += b.n;
     return true;
@@ -214,9 +215,9 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
   const size_t plane = size_t(H) * W;
   const float* __restrict__ uin_all = ((iter - 1) & 1) ? a.buf1 : a.buf0;
   float* __restrict__ uout_all = (iter & 1) ? a.buf1 : a.buf0;
-  const int64_t L0 = cta_start(blockIdx.x, a.pt.S, a.pt.G);
-  const int64_t L1 = cta_start(blockIdx.x + 1, a.pt.S, a.pt.G);
-  int64_t L = L0;
+  const int L0 = int(cta_start(blockIdx.x, a.pt.S, a.pt.G));
+  const int L1 = int(cta_start(blockIdx.x + 1, a.pt.S, a.pt.G));
+  int L = L0;
 
   SBlock cur, nxt;
   bool have = next_block(L, L0, L1, a, iter, cur);
@@ -247,14 +248,18 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
     // ---- prefetch Phi / lambda for this thread's outputs into registers
     float2 phv[8], lmv[8];
     {
-      const float* __restrict__ ph = a.phi + cur.p * plane;
-      const float* __restrict__ lm = a.lam + (cur.p / a.C) * plane;
+      const size_t off0 = size_t(cur.yb + j0) * W + gx;
+      const float2* __restrict__ ph =
+          reinterpret_cast<const float2*>(a.phi + cur.p * plane + off0);
+      const float2* __restrict__ lm =
+          reinterpret_cast<const float2*>(a.lam + (cur.p / a.C) * plane + off0);
+      const int rows_here = col_ok ? min(8, cur.n - j0) : 0;
+      const int w2 = W >> 1;  // row stride in float2
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int y = cur.yb + j0 + j;
-        if (col_ok && j0 + j < cur.n) {
-          phv[j] = __ldg(reinterpret_cast<const float2*>(ph + size_t(y) * W + gx));
-          lmv[j] = __ldg(reinterpret_cast<const float2*>(lm + size_t(y) * W + gx));
+        if (j < rows_here) {
+          phv[j] = __ldg(ph + j * w2);
+          lmv[j] = __ldg(lm + j * w2);
         } else {
           phv[j] = make_float2(0.f, 0.f);
           lmv[j] = make_float2(0.f, 0.f);
@@ -274,14 +279,16 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
     const int nnew = cur.first ? cur.n + 2 * R : cur.n;
     const int xbase = cur.x0 - Gm::RP;  // global column of staged column 0
     if (xbase < 0 || xbase + Gm::PWD > W) {
-      for (int k = tid; k < nnew * Gm::PWD; k += kComputeThreads) {
-        const int i = k / Gm::PWD, ci = k - i * Gm::PWD;
-        const int g = xbase + ci;
-        if (g < 0 || g >= W) {
-          const int src = reflect(g, W) - xbase;
-          if (src >= 0 && src < Gm::PWD)
-            in_cur[(new0 + i) * Gm::PITCH + ci] = in_cur[(new0 + i) * Gm::PITCH + src];
-        }
+      // only the out-of-image staged columns: [0, nl) on the left, [cr, PWD) on the right
+      const int nl = xbase < 0 ? -xbase : 0;
+      const int cr = min(Gm::PWD, max(nl, W - xbase));
+      const int nh = nl + (Gm::PWD - cr);
+      for (int k = tid; k < nnew * nh; k += kComputeThreads) {
+        const int i = k / nh, h = k - i * nh;
+        const int ci = h < nl ? h : cr + (h - nl);
+        const int src = reflect(xbase + ci, W) - xbase;
+        if (src >= 0 && src < Gm::PWD)
+          in_cur[(new0 + i) * Gm::PITCH + ci] = in_cur[(new0 + i) * Gm::PITCH + src];
       }
     }
     compute_bar();
@@ -317,10 +324,14 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
       hn = cur.n;
       in0row = R + 1;
     }
-    for (int item = tid; item < hn * (kSTW / 4); item += kComputeThreads) {
-      const int i = item >> 4, g = item & 15;
-      const float* row = in_cur + (in0row + i) * Gm::PITCH + 4 * g;
-      constexpr int NQ = (Gm::RP + R + 3) / 4 + 1;
+    // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R) staged
+    // values per 8 outputs.  Lanes 0-7 of a quarter-warp cover one row's 64
+    // columns (8 x 32 B) so the float4 loads are bank-conflict free.
+    for (int item = tid; item < hn * (kSTW / 8); item += kComputeThreads) {
+      const int i = item >> 3, g = item & 7;
+      const float* row = in_cur + (in0row + i) * Gm::PITCH + 8 * g;
+      constexpr int OFF = Gm::RP - R;
+      constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
       float v[4 * NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -330,17 +341,18 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
       }
-      constexpr int OFF = Gm::RP - R;
-      float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+      float o[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) o[m] = 0.f;
 #pragma unroll
       for (int k = 0; k <= 2 * R; ++k) {
         const float wk = a.w[k];
-        o0 = fmaf(wk, v[OFF + k], o0);
-        o1 = fmaf(wk, v[OFF + k + 1], o1);
-        o2 = fmaf(wk, v[OFF + k + 2], o2);
-        o3 = fmaf(wk, v[OFF + k + 3], o3);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) o[m] = fmaf(wk, v[OFF + k + m], o[m]);
       }
-      reinterpret_cast<float4*>(h_cur + (hnew0 + i) * kSTW)[g] = make_float4(o0, o1, o2, o3);
+      float4* dst = reinterpret_cast<float4*>(h_cur + (hnew0 + i) * kSTW + 8 * g);
+      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
     }
     compute_bar();
 

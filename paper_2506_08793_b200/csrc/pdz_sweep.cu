@@ -359,7 +359,9 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
   const bool edge = p->edge_preserving != 0;
   size_t smem = 0;
   StreamFn sfn = nullptr;
-  if (!g_force_tiled && p->width % 4 == 0)
+  const int64_t strip_rows =
+      int64_t((p->width + kSTW - 1) / kSTW) * p->height * int64_t(p->planes);
+  if (!g_force_tiled && p->width % 4 == 0 && strip_rows < (int64_t(1) << 31))
     sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
   if (sfn) {
     P.stream = true;
