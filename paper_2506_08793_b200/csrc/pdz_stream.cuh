@@ -134,32 +134,51 @@ struct SBlock {
   int p, x0, yb, n, first;
 };
 
-// Next block of this CTA's range; skips planes frozen at <= iter-2.
-// (32-bit arithmetic: the host only selects this kernel when S < 2^31.)
-__device__ __forceinline__ bool next_block(int& L, int L0, int L1, const StreamArgs& a,
-                                           int iter, SBlock& b) {
-  while (L < L1) {
-    const int u = L / a.H;
-    const int y = L - u * a.H;
-    const int seg_end = min(L1, (u + 1) * a.H);
-    const int p = u / a.nstrips;
-    if (a.st.stop_iter) {
-      const int s = a.st.stop_iter[p];
-      if (s != 0 && s < iter - 1) {
-        L = seg_end;
-        continue;
-      }
-    }
-    b.p = p;
-    b.x0 = (u - p * a.nstrips) * kSTW;
-    b.yb = y;
-    b.n = min(kSRB, seg_end - L);
-    b.first = (L == L0) || (y == 0);
-    L += b.n;
-    return true;
+// Walks a CTA's range [L0, L1) of strip-rows block by block: (plane p, strip
+// s, row y) advance incrementally, so only the start needs divisions.  Planes
+// frozen at <= iter-2 are skipped.  (32-bit: the host only selects this
+// kernel when S < 2^31.)
+struct RangeIter {
+  int L, L0, L1, p, s, y;
+  __device__ __forceinline__ void init(int l0, int l1, const StreamArgs& a) {
+    L = L0 = l0;
+    L1 = l1;
+    const int u = l0 / a.H;
+    y = l0 - u * a.H;
+    p = u / a.nstrips;
+    s = u - p * a.nstrips;
   }
-  return false;
-}
+  __device__ __forceinline__ void wrap(const StreamArgs& a) {
+    y = 0;
+    if (++s == a.nstrips) {
+      s = 0;
+      ++p;
+    }
+  }
+  __device__ __forceinline__ bool next(const StreamArgs& a, int iter, SBlock& b) {
+    while (L < L1) {
+      const int seg_end = min(L1, L - y + a.H);
+      if (a.st.stop_iter) {
+        const int st = a.st.stop_iter[p];
+        if (st != 0 && st < iter - 1) {
+          L = seg_end;
+          wrap(a);
+          continue;
+        }
+      }
+      b.p = p;
+      b.x0 = s * kSTW;
+      b.yb = y;
+      b.n = min(kSRB, seg_end - L);
+      b.first = (L == L0) || (y == 0);
+      L += b.n;
+      y += b.n;
+      if (y == a.H) wrap(a);
+      return true;
+    }
+    return false;
+  }
+};
 
 // Warp 0 of the compute warps: queue the bulk copies of the block's new input
 // rows (reflected row indices, in-image column span) into `in`.
@@ -215,12 +234,12 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
   const size_t plane = size_t(H) * W;
   const float* __restrict__ uin_all = ((iter - 1) & 1) ? a.buf1 : a.buf0;
   float* __restrict__ uout_all = (iter & 1) ? a.buf1 : a.buf0;
-  const int L0 = int(cta_start(blockIdx.x, a.pt.S, a.pt.G));
-  const int L1 = int(cta_start(blockIdx.x + 1, a.pt.S, a.pt.G));
-  int L = L0;
+  RangeIter it;
+  it.init(int(cta_start(blockIdx.x, a.pt.S, a.pt.G)),
+          int(cta_start(blockIdx.x + 1, a.pt.S, a.pt.G)), a);
 
   SBlock cur, nxt;
-  bool have = next_block(L, L0, L1, a, iter, cur);
+  bool have = it.next(a, iter, cur);
   if (have && warp == 0)
     issue_rows<R>(cur, uin_all + cur.p * plane, in0, &bars[0], H, W, lane);
 
@@ -233,8 +252,16 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
   float acc_nf = 0.0f;
   int acc_p = have ? cur.p : -1;
 
+  // One CTA barrier per block:
+  //   wait IN(b) [+ border fix-up + barrier, border strips only]
+  //   -> carry H overlap, blur the new rows into H(b)
+  //   -> barrier
+  //   -> carry the IN overlap into the other buffer, queue IN(b+1),
+  //      vertical pass + divergence + update of block b.
+  // H(b) is written while only H(b-1) is read; IN(b+1) overwrites the buffer
+  // last read by block b-1, which every thread finished before the barrier.
   while (have) {
-    const bool have_nxt = next_block(L, L0, L1, a, iter, nxt);
+    const bool have_nxt = it.next(a, iter, nxt);
     float* const in_cur = ib ? in1 : in0;
     float* const in_nxt = ib ? in0 : in1;
     float* const h_cur = ib ? h1 : h0;
@@ -243,7 +270,6 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
     uint64_t* const bar_nxt = &bars[ib ^ 1];
     const int gx = cur.x0 + c;
     const bool col_ok = gx < W;
-    const float* __restrict__ uin = uin_all + cur.p * plane;
 
     // ---- prefetch Phi / lambda for this thread's outputs into registers
     float2 phv[8], lmv[8];
@@ -275,10 +301,10 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
       mbar_wait(bar_cur, phase0);
       phase0 ^= 1;
     }
-    const int new0 = cur.first ? 0 : R + 1;
-    const int nnew = cur.first ? cur.n + 2 * R : cur.n;
     const int xbase = cur.x0 - Gm::RP;  // global column of staged column 0
-    if (xbase < 0 || xbase + Gm::PWD > W) {
+    if (xbase < 0 || xbase + Gm::PWD > W) {  // border strip (CTA-uniform)
+      const int new0 = cur.first ? 0 : R + 1;
+      const int nnew = cur.first ? cur.n + 2 * R : cur.n;
       // only the out-of-image staged columns: [0, nl) on the left, [cr, PWD) on the right
       const int nl = xbase < 0 ? -xbase : 0;
       const int cr = min(Gm::PWD, max(nl, W - xbase));
@@ -290,24 +316,7 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
         if (src >= 0 && src < Gm::PWD)
           in_cur[(new0 + i) * Gm::PITCH + ci] = in_cur[(new0 + i) * Gm::PITCH + src];
       }
-    }
-    compute_bar();
-
-    // ---- queue the next block's rows (+ carry of the R+1 overlap rows)
-    if (have_nxt) {
-      if (!nxt.first) {
-        // rows [nxt.yb - 1, nxt.yb + R) live in in_cur at idx (row - cur_base)
-        const int cur_base = cur.first ? cur.yb - R : cur.yb - 1;
-        const int s0 = (nxt.yb - 1) - cur_base;
-        const int nf4 = (R + 1) * (Gm::PWD / 4);
-        for (int k = tid; k < nf4; k += kComputeThreads) {
-          const int i = k / (Gm::PWD / 4), q = k - i * (Gm::PWD / 4);
-          reinterpret_cast<float4*>(in_nxt + i * Gm::PITCH)[q] =
-              reinterpret_cast<const float4*>(in_cur + (s0 + i) * Gm::PITCH)[q];
-        }
-      }
-      if (warp == 0)
-        issue_rows<R>(nxt, uin_all + nxt.p * plane, in_nxt, bar_nxt, H, W, lane);
+      compute_bar();
     }
 
     // ---- H rows: carry the 2R overlap, blur the new rows
@@ -325,8 +334,7 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
       in0row = R + 1;
     }
     // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R) staged
-    // values per 8 outputs.  Lanes 0-7 of a quarter-warp cover one row's 64
-    // columns (8 x 32 B) so the float4 loads are bank-conflict free.
+    // values per 8 outputs.
     for (int item = tid; item < hn * (kSTW / 8); item += kComputeThreads) {
       const int i = item >> 3, g = item & 7;
       const float* row = in_cur + (in0row + i) * Gm::PITCH + 8 * g;
@@ -355,6 +363,23 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
       dst[1] = make_float4(o[4], o[5], o[6], o[7]);
     }
     compute_bar();
+
+    // ---- queue the next block's rows (+ carry of the R+1 overlap rows)
+    if (have_nxt) {
+      if (!nxt.first) {
+        // rows [nxt.yb - 1, nxt.yb + R) live in in_cur at idx (row - cur_base)
+        const int cur_base = cur.first ? cur.yb - R : cur.yb - 1;
+        const int s0 = (nxt.yb - 1) - cur_base;
+        constexpr int Q = Gm::PWD / 4;
+        for (int k = tid; k < (R + 1) * Q; k += kComputeThreads) {
+          const int i = k / Q, q = k - i * Q;
+          reinterpret_cast<float4*>(in_nxt + i * Gm::PITCH)[q] =
+              reinterpret_cast<const float4*>(in_cur + (s0 + i) * Gm::PITCH)[q];
+        }
+      }
+      if (warp == 0)
+        issue_rows<R>(nxt, uin_all + nxt.p * plane, in_nxt, bar_nxt, H, W, lane);
+    }
 
     // ---- vertical pass (FFMA2 over the column pair), divergence, update
     if (j0 < cur.n) {
