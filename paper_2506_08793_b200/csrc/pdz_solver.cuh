@@ -29,6 +29,7 @@ struct Partials {
   double* sum;
   int32_t* flag;
   int32_t nbmax;
+  int32_t ring;   // iteration slots: iteration it uses slot it % ring
   // v1: count = tiles (fixed); v2: count = hi(p) - lo(p) + 1 with CTA ranges
   int32_t tiles;
   int64_t S;      // v2: total strip-rows
@@ -63,7 +64,7 @@ __device__ __forceinline__ void finalize_iteration_warp(const StateView& st, con
   int running = 0;
   for (int p = lane; p < P; p += 32) {
     if (st.stop_iter[p] != 0) continue;
-    const size_t base = (size_t(it & 1) * P + p) * pt.nbmax;
+    const size_t base = (size_t(it % pt.ring) * P + p) * pt.nbmax;
     const int n = partial_count(pt, p);
     double s = 0.0;
     int nf = 0;

@@ -272,7 +272,7 @@ __global__ void init_state_kernel(StateView st, int P) {
 // Single fixed_point_step: norms[p] = sqrt(sum of the iteration-1 partials).
 __global__ void step_norm_kernel(Partials pt, int P, double* norms, int32_t* nonfinite) {
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    const size_t base = (size_t(1) * P + p) * pt.nbmax;
+    const size_t base = (size_t(1 % pt.ring) * P + p) * pt.nbmax;
     const int n = partial_count(pt, p);
     double s = 0.0;
     int nf = 0;
@@ -319,8 +319,9 @@ static SweepFn pick_kernel(int R) {
   }
 }
 
-// How one sweep is launched: the streaming kernel (width % 4 == 0 and a
-// compiled radius) or the tiled fallback.
+// How a solve is launched: the persistent streaming kernel (width % 4 == 0,
+// a compiled radius, S < 2^31) as one cooperative launch, or the tiled
+// fallback as graph-replayed per-sweep launches.
 struct Plan {
   bool stream = false;
   int R = 1;
@@ -328,6 +329,7 @@ struct Plan {
   int G = 0, nstrips = 0;                   // streaming
   int64_t S = 0, U = 0;
   int nbmax = 0;                            // partial slots per plane
+  int ring = 2;                             // iteration slots of the partials
   size_t smem = 0;
   void* fn = nullptr;
 };
@@ -363,16 +365,16 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
       int64_t((p->width + kSTW - 1) / kSTW) * p->height * int64_t(p->planes);
   if (!g_force_tiled && p->width % 4 == 0 && strip_rows < (int64_t(1) << 31))
     sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
-  if (sfn) {
+  int occ = 0;
+  if (sfn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
+  if (sfn && occ >= 1) {
     P.stream = true;
     P.fn = reinterpret_cast<void*>(sfn);
     P.smem = smem;
+    P.ring = kRing;
     P.nstrips = (p->width + kSTW - 1) / kSTW;
     P.U = int64_t(P.nstrips) * p->height;
     P.S = P.U * p->planes;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
-    occ = std::max(1, occ);
     const int64_t gmax = int64_t(num_sms()) * occ;
     P.G = int(std::max<int64_t>(1, std::min<int64_t>(gmax, P.S / 16)));
     int nb = 1;
@@ -383,9 +385,11 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
     }
     P.nbmax = nb;
   } else {
+    cudaGetLastError();  // clear a failed occupancy query
     P.stream = false;
     P.fn = reinterpret_cast<void*>(edge ? pick_kernel<true>(P.R) : pick_kernel<false>(P.R));
     P.smem = tile_smem(P.R);
+    P.ring = 2;
     P.tiles_x = (p->width + kTW - 1) / kTW;
     P.tiles_y = (p->height + kTH - 1) / kTH;
     P.nblk = P.tiles_x * P.tiles_y;
@@ -400,9 +404,15 @@ struct LaunchArgs {
   StreamArgs stream;
 };
 
+struct Sync {
+  int32_t* done;   // [G]
+  int32_t* fin;    // [1]
+  int32_t* flags;  // [2]
+};
+
 static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0, float* buf1,
                          const float* phi, const float* lam, double* psum, int32_t* pflag,
-                         const StateView& st, LaunchArgs* la) {
+                         const StateView& st, const Sync& sy, LaunchArgs* la) {
   memset(la, 0, sizeof(*la));
   double taps[kMaxTaps];
   int32_t rc = gaussian_taps_host(p->sigma, p->kernel_size, taps);
@@ -418,6 +428,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   pt.sum = psum;
   pt.flag = pflag;
   pt.nbmax = pl.nbmax;
+  pt.ring = pl.ring;
   pt.tiles = pl.stream ? 0 : pl.nblk;
   pt.S = pl.S;
   pt.U = pl.U;
@@ -448,12 +459,18 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.lam = lam;
   b.pt = pt;
   b.st = st;
+  b.done = sy.done;
+  b.fin = sy.fin;
+  b.flags = sy.flags;
   b.H = p->height;
   b.W = p->width;
   b.P = p->planes;
   b.C = p->channels;
   b.nstrips = pl.nstrips;
+  b.iter_first = 1;
+  b.iter_last = p->max_iters;
   b.max_iters = p->max_iters;
+  b.stop_rule = (p->rel_tol >= 0.0) ? 1 : 0;
   b.eps = float(p->epsilon);
   b.tau = float(p->tau);
   b.rel_tol = p->rel_tol;
@@ -461,7 +478,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   return PDZ_OK;
 }
 
-static int32_t launch_sweep(LaunchArgs la, const pdz_solve_params* p, const Plan& pl,
+static int32_t launch_tiled(LaunchArgs la, const pdz_solve_params* p, const Plan& pl,
                             int iter_off, cudaStream_t s, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = s;
@@ -471,20 +488,40 @@ static int32_t launch_sweep(LaunchArgs la, const pdz_solve_params* p, const Plan
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (pl.stream) {
-    la.stream.iter_off = iter_off;
-    cfg.gridDim = dim3(pl.G);
-    cfg.blockDim = dim3(kSThreads);
-    PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<StreamFn>(pl.fn), la.stream),
-             "stream sweep launch");
-  } else {
-    la.tile.iter_off = iter_off;
-    cfg.gridDim = dim3(pl.tiles_x, pl.tiles_y, p->planes);
-    cfg.blockDim = dim3(kThreads);
-    PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<SweepFn>(pl.fn), la.tile),
-             "tiled sweep launch");
-  }
+  la.tile.iter_off = iter_off;
+  cfg.gridDim = dim3(pl.tiles_x, pl.tiles_y, p->planes);
+  cfg.blockDim = dim3(kThreads);
+  PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<SweepFn>(pl.fn), la.tile),
+           "tiled sweep launch");
   return PDZ_OK;
+}
+
+// All sweeps of a streaming solve: one cooperative launch (co-residency of the
+// G CTAs is what makes the neighbour waits deadlock-free).
+static int32_t launch_stream(const LaunchArgs& la, const Plan& pl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = s;
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.gridDim = dim3(pl.G);
+  cfg.blockDim = dim3(kSThreads);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<StreamFn>(pl.fn), la.stream),
+           "persistent sweep launch");
+  return PDZ_OK;
+}
+
+__global__ void sync_init_kernel(Sync sy, int G) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x)
+    sy.done[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sy.fin[0] = 0;
+    sy.flags[0] = 0;
+    sy.flags[1] = 0;
+  }
 }
 
 struct SolveLayout {
@@ -493,6 +530,7 @@ struct SolveLayout {
   double* psum;
   int32_t* pflag;
   StateView st;
+  Sync sy;
   size_t bytes;
 };
 
@@ -503,8 +541,8 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   const size_t P = p->planes;
   L.buf0 = c.take<float>(P * plane);
   L.buf1 = c.take<float>(P * plane);
-  L.psum = c.take<double>(2 * P * pl.nbmax);
-  L.pflag = c.take<int32_t>(2 * P * pl.nbmax);
+  L.psum = c.take<double>(size_t(pl.ring) * P * pl.nbmax);
+  L.pflag = c.take<int32_t>(size_t(pl.ring) * P * pl.nbmax);
   L.st.stop_iter = c.take<int32_t>(P);
   L.st.converged = c.take<int32_t>(P);
   L.st.failed = c.take<int32_t>(P);
@@ -514,11 +552,15 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   L.st.running = c.take<int32_t>(1);
   L.st.iter_base = c.take<int32_t>(1);
   L.st.chunk_ctr = c.take<int32_t>(1);
+  L.sy.done = c.take<int32_t>(std::max(1, pl.G));
+  L.sy.fin = c.take<int32_t>(1);
+  L.sy.flags = c.take<int32_t>(2);
   L.bytes = c.off;
   return L;
 }
 
-// Graph cache: one instantiated chunk graph per (args, params, stream).
+// Graph cache for the tiled path: one instantiated chunk graph per
+// (args, params, stream).
 struct GraphKey {
   std::vector<unsigned char> bytes;
   bool operator<(const GraphKey& o) const { return bytes < o.bytes; }
@@ -529,10 +571,10 @@ static std::map<GraphKey, cudaGraphExec_t> g_graphs;
 static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, const Plan& pl,
                            cudaStream_t s, cudaGraphExec_t* out) {
   GraphKey key;
-  key.bytes.resize(sizeof(LaunchArgs) + sizeof(pdz_solve_params) + sizeof(void*));
-  memcpy(key.bytes.data(), &la, sizeof(LaunchArgs));
-  memcpy(key.bytes.data() + sizeof(LaunchArgs), p, sizeof(pdz_solve_params));
-  memcpy(key.bytes.data() + sizeof(LaunchArgs) + sizeof(pdz_solve_params), &s, sizeof(void*));
+  key.bytes.resize(sizeof(SweepArgs) + sizeof(pdz_solve_params) + sizeof(void*));
+  memcpy(key.bytes.data(), &la.tile, sizeof(SweepArgs));
+  memcpy(key.bytes.data() + sizeof(SweepArgs), p, sizeof(pdz_solve_params));
+  memcpy(key.bytes.data() + sizeof(SweepArgs) + sizeof(pdz_solve_params), &s, sizeof(void*));
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     auto it = g_graphs.find(key);
@@ -547,7 +589,7 @@ static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, cons
   PDZ_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   chunk_base_kernel<<<1, 1, 0, cap>>>(la.tile.st);
   int32_t rc = PDZ_OK;
-  for (int i = 0; i < kChunk && rc == PDZ_OK; ++i) rc = launch_sweep(la, p, pl, i, cap, true);
+  for (int i = 0; i < kChunk && rc == PDZ_OK; ++i) rc = launch_tiled(la, p, pl, i, cap, true);
   cudaError_t e = cudaStreamEndCapture(cap, &graph);
   cudaStreamDestroy(cap);
   if (rc != PDZ_OK) return rc;
@@ -567,25 +609,29 @@ static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, cons
   return PDZ_OK;
 }
 
-// Queue init + all sweeps (graph chunks) on the stream.  With `poll` the host
-// watches the device `running` counter (lagged by one chunk) and stops
-// queueing once every plane has stopped.
+// Queue init + all sweeps on the stream.  Streaming: one persistent launch
+// that stops by itself once every plane has stopped.  Tiled: graph chunks;
+// with `poll` the host watches the device `running` counter (lagged by one
+// chunk) and stops queueing once every plane has stopped.
 static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
-                           const float* phi, const float* lam, cudaStream_t s, bool poll,
-                           int* last_iter) {
+                           const float* phi, const float* lam, cudaStream_t s, bool poll) {
   LaunchArgs la;
-  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, phi, lam, L.psum, L.pflag, L.st, &la);
+  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, phi, lam, L.psum, L.pflag, L.st, L.sy, &la);
   if (rc != PDZ_OK) return rc;
   const size_t plane_bytes = size_t(p->height) * p->width * sizeof(float);
   PDZ_CUDA(cudaMemcpyAsync(L.buf0, phi, plane_bytes * p->planes, cudaMemcpyDeviceToDevice, s),
            "u0 = Phi");
   init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
   PDZ_CHECK_LAUNCH("init state");
+  if (pl.stream) {
+    sync_init_kernel<<<(pl.G + 255) / 256, 256, 0, s>>>(L.sy, pl.G);
+    PDZ_CHECK_LAUNCH("sync init");
+    return launch_stream(la, pl, s);
+  }
 
   cudaGraphExec_t exec;
   rc = chunk_graph(la, p, pl, s, &exec);
   if (rc != PDZ_OK) return rc;
-
   const int n_chunks = (p->max_iters + kChunk - 1) / kChunk;
   static thread_local int32_t* pinned = nullptr;
   static thread_local cudaEvent_t events[2] = {nullptr, nullptr};
@@ -624,7 +670,17 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   PDZ_CUDA(cudaLaunchKernelEx(&cfg, finalize_kernel, L.st, pt, int(p->planes), launched,
                               int(p->max_iters), p->rel_tol),
            "finalize launch");
-  *last_iter = launched;
+  return PDZ_OK;
+}
+
+static int32_t check_abort(const Plan& pl, const Sync& sy) {
+  if (!pl.stream) return PDZ_OK;
+  int32_t f[2] = {0, 0};
+  PDZ_CUDA(cudaMemcpy(f, sy.flags, sizeof(f), cudaMemcpyDeviceToHost), "D2H flags");
+  if (f[1]) {
+    set_error("persistent sweep aborted: a CTA dependency wait timed out");
+    return PDZ_ECUDA;
+  }
   return PDZ_OK;
 }
 
@@ -634,13 +690,20 @@ using namespace pdz;
 
 extern "C" {
 
+static size_t step_bytes(const pdz_solve_params* params, const Plan& pl) {
+  Carver c(nullptr, 0);
+  c.take<double>(size_t(pl.ring) * params->planes * pl.nbmax);
+  c.take<int32_t>(size_t(pl.ring) * params->planes * pl.nbmax);
+  c.take<int32_t>(std::max(1, pl.G));
+  c.take<int32_t>(1);
+  c.take<int32_t>(2);
+  return Carver::round(c.off);
+}
+
 size_t pdz_step_workspace_bytes(const pdz_solve_params* params) {
   Plan pl;
   if (check_params(params, &pl) != PDZ_OK) return 0;
-  Carver c(nullptr, 0);
-  c.take<double>(2 * size_t(params->planes) * pl.nbmax);
-  c.take<int32_t>(2 * size_t(params->planes) * pl.nbmax);
-  return Carver::round(c.off);
+  return step_bytes(params, pl);
 }
 
 int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, float* u_out,
@@ -653,8 +716,12 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
   PDZ_REQUIRE(u && u_out && phi && lambda_map && norms, "NULL array argument");
   PDZ_REQUIRE(u != u_out, "u_out must not alias u");
   Carver c(workspace, workspace_bytes);
-  double* psum = c.take<double>(2 * size_t(params->planes) * pl.nbmax);
-  int32_t* pflag = c.take<int32_t>(2 * size_t(params->planes) * pl.nbmax);
+  double* psum = c.take<double>(size_t(pl.ring) * params->planes * pl.nbmax);
+  int32_t* pflag = c.take<int32_t>(size_t(pl.ring) * params->planes * pl.nbmax);
+  Sync sy;
+  sy.done = c.take<int32_t>(std::max(1, pl.G));
+  sy.fin = c.take<int32_t>(1);
+  sy.flags = c.take<int32_t>(2);
   if (!c.ok) {
     set_error("workspace too small: need %zu bytes, got %zu", c.off, workspace_bytes);
     return PDZ_EWORKSPACE;
@@ -663,11 +730,18 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
   one.max_iters = 1;
   LaunchArgs la;
   StateView none = {};
-  rc = fill_args(&one, pl, const_cast<float*>(u), u_out, phi, lambda_map, psum, pflag, none,
-                 &la);  // iteration 1 reads buf0 (= u), writes buf1 (= u_out)
+  // iteration 1 reads buf0 (= u), writes buf1 (= u_out)
+  rc = fill_args(&one, pl, const_cast<float*>(u), u_out, phi, lambda_map, psum, pflag, none, sy,
+                 &la);
   if (rc != PDZ_OK) return rc;
   cudaStream_t s = as_stream(stream);
-  rc = launch_sweep(la, &one, pl, 1, s, false);
+  if (pl.stream) {
+    sync_init_kernel<<<1, 256, 0, s>>>(sy, pl.G);
+    PDZ_CHECK_LAUNCH("sync init");
+    rc = launch_stream(la, pl, s);
+  } else {
+    rc = launch_tiled(la, &one, pl, 1, s, false);
+  }
   if (rc != PDZ_OK) return rc;
   step_norm_kernel<<<1, 256, 0, s>>>(la.tile.pt, params->planes, norms, nonfinite);
   PDZ_CHECK_LAUNCH("step norm");
@@ -697,11 +771,12 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
     return PDZ_EWORKSPACE;
   }
   cudaStream_t s = as_stream(stream);
-  int last = 0;
-  rc = queue_solve(params, pl, L, phi, lambda_map, s, true, &last);
+  rc = queue_solve(params, pl, L, phi, lambda_map, s, true);
   if (rc != PDZ_OK) return rc;
   const int P = params->planes;
   PDZ_CUDA(cudaStreamSynchronize(s), "solve sync");
+  rc = check_abort(pl, L.sy);
+  if (rc != PDZ_OK) return rc;
   PDZ_CUDA(cudaMemcpy(iterations_host, L.st.iters, P * 4, cudaMemcpyDeviceToHost), "D2H iters");
   PDZ_CUDA(cudaMemcpy(converged_host, L.st.converged, P * 4, cudaMemcpyDeviceToHost), "D2H conv");
   PDZ_CUDA(cudaMemcpy(failed_host, L.st.failed, P * 4, cudaMemcpyDeviceToHost), "D2H failed");
@@ -741,12 +816,13 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
     set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
-  int last = 0;
-  return queue_solve(&fixed, pl, L, phi, lambda_map, as_stream(stream), false, &last);
+  return queue_solve(&fixed, pl, L, phi, lambda_map, as_stream(stream), false);
 }
 
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {
-  if (check_params(params, nullptr) != PDZ_OK) return -1;
+  Plan pl;
+  if (check_params(params, &pl) != PDZ_OK) return -1;
+  if (pl.stream) return 3;  // init state + sync init + one persistent launch
   const int64_t chunks = (params->max_iters + kChunk - 1) / kChunk;
   return 2 + chunks * (1 + kChunk);  // init + chunk prologues + sweeps + finalize
 }
