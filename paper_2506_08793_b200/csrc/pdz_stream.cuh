@@ -123,6 +123,16 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Polling load: relaxed (no L1 invalidation per poll); the caller issues one
+// acquire fence once the condition holds.
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -241,12 +251,15 @@ __device__ bool wait_deps(const StreamArgs& a, int lo, int hi, int need_done, in
   unsigned ns = 32;
   while (true) {
     bool ok = true;
-    for (int j = lo + lane; j <= hi; j += 32) ok &= ld_acquire(a.done + j) >= need_done;
-    if (lane == 0 && need_fin > 0) ok &= ld_acquire(a.fin) >= need_fin;
+    for (int j = lo + lane; j <= hi; j += 32) ok &= ld_relaxed(a.done + j) >= need_done;
+    if (lane == 0 && need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
     ok = __all_sync(0xffffffffu, ok);
-    const int stop = ld_acquire(a.flags) | ld_acquire(a.flags + 1);
+    const int stop = ld_relaxed(a.flags) | ld_relaxed(a.flags + 1);
     if (__any_sync(0xffffffffu, stop != 0)) return false;
-    if (ok) return true;
+    if (ok) {
+      fence_acquire_gpu();
+      return true;
+    }
     if (global_ns() - t0 > kSpinTimeoutNs) {
       if (lane == 0) atomicExch(a.flags + 1, 1);
       return false;
@@ -265,10 +278,13 @@ __device__ void service_loop(const StreamArgs& a) {
     unsigned ns = 64;
     while (true) {
       bool ok = true;
-      for (int j = lane; j < G; j += 32) ok &= ld_acquire(a.done + j) >= m;
+      for (int j = lane; j < G; j += 32) ok &= ld_relaxed(a.done + j) >= m;
       ok = __all_sync(0xffffffffu, ok);
-      if (ok) break;
-      if (__any_sync(0xffffffffu, ld_acquire(a.flags + 1) != 0)) return;
+      if (ok) {
+        fence_acquire_gpu();
+        break;
+      }
+      if (__any_sync(0xffffffffu, ld_relaxed(a.flags + 1) != 0)) return;
       if (global_ns() - t0 > kSpinTimeoutNs) {
         if (lane == 0) atomicExch(a.flags + 1, 1);
         return;
@@ -591,9 +607,12 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
       ib ^= 1;
     }
     // ---- publish: every output row and partial of this sweep is written
-    __threadfence();
+    // (barrier orders the CTA's writes before thread 0's cumulative fence)
     compute_bar();
-    if (tid == 0) st_release(a.done + blockIdx.x, iter);
+    if (tid == 0) {
+      __threadfence();
+      st_release(a.done + blockIdx.x, iter);
+    }
   }
 }
 

@@ -375,8 +375,20 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
     P.nstrips = (p->width + kSTW - 1) / kSTW;
     P.U = int64_t(P.nstrips) * p->height;
     P.S = P.U * p->planes;
+    // Grid size: all CTAs co-resident (cooperative), and CTA ranges aligned to
+    // strip boundaries so every CTA pays the same segment-start halo: k CTAs
+    // per strip when strips are fewer than slots, else ~equal strips per CTA.
     const int64_t gmax = int64_t(num_sms()) * occ;
-    P.G = int(std::max<int64_t>(1, std::min<int64_t>(gmax, P.S / 16)));
+    const int64_t units = int64_t(P.nstrips) * p->planes;
+    int64_t G;
+    if (units <= gmax) {
+      const int64_t k = std::max<int64_t>(1, std::min<int64_t>(gmax / units, p->height / 16));
+      G = units * k;
+    } else {
+      const int64_t m = (units + gmax - 1) / gmax;  // strips per CTA
+      G = (units + m - 1) / m;
+    }
+    P.G = int(std::max<int64_t>(1, G));
     int nb = 1;
     for (int q = 0; q < p->planes; ++q) {
       const int64_t lo = cta_of(int64_t(q) * P.U, P.S, P.G);
