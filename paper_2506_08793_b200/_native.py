@@ -25,7 +25,8 @@ __all__ = [
     "LAMBDA_MODES_C",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpdz.so")
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        os.environ.get("PDZ_LIB_NAME", "libpdz.so"))  # libpdz_prof.so: profiling
 
 PDZ_OK, PDZ_EINVAL, PDZ_ENONFINITE, PDZ_ECUDA, PDZ_EWORKSPACE = 0, 1, 2, 3, 4
 

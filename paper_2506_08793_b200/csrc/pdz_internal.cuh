@@ -66,6 +66,9 @@ struct Carver {
 // np.pad(mode="symmetric") source index with repeated reflection
 // (solver.py:235): fold modulo 2n, mirror the upper half.
 __host__ __device__ __forceinline__ int reflect(int i, int n) {
+  if (i >= 0 && i < n) return i;               // fast paths: at most one fold
+  if (i < 0 && i >= -n) return -1 - i;
+  if (i >= n && i < 2 * n) return 2 * n - 1 - i;
   int m = i % (2 * n);
   if (m < 0) m += 2 * n;
   return m >= n ? 2 * n - 1 - m : m;

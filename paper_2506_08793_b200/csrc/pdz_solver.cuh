@@ -32,9 +32,10 @@ struct Partials {
   int32_t ring;   // iteration slots: iteration it uses slot it % ring
   // v1: count = tiles (fixed); v2: count = hi(p) - lo(p) + 1 with CTA ranges
   int32_t tiles;
-  int64_t S;      // v2: total strip-rows
-  int64_t U;      // v2: strip-rows per plane
+  int64_t S;      // v2: total strip-rows (images x strips x H)
+  int64_t U;      // v2: strip-rows per image (strips x H)
   int32_t G;      // v2: grid size
+  int32_t C;      // v2: planes per image (the C channels share the CTA ranges)
 };
 
 // Index of the CTA whose balanced range [floor(iS/G), floor((i+1)S/G)) holds
@@ -48,20 +49,66 @@ __host__ __device__ __forceinline__ int64_t cta_start(int64_t i, int64_t S, int6
 
 __device__ __forceinline__ int partial_count(const Partials& pt, int p) {
   if (pt.tiles > 0) return pt.tiles;
-  const int64_t lo = cta_of(int64_t(p) * pt.U, pt.S, pt.G);
-  const int64_t hi = cta_of(int64_t(p + 1) * pt.U - 1, pt.S, pt.G);
+  const int64_t img = p / pt.C;
+  const int64_t lo = cta_of(img * pt.U, pt.S, pt.G);
+  const int64_t hi = cta_of((img + 1) * pt.U - 1, pt.S, pt.G);
   return int(hi - lo + 1);
 }
 
+// Apply the stop rule of fixed_point_solve (solver.py:347-358) to plane p
+// given iteration `it`'s reduced sum of r^2; returns 1 if p keeps running.
+__device__ __forceinline__ int finalize_plane(const StateView& st, int P, int p, int it,
+                                              int max_iters, double rel_tol, double s, int nf) {
+  if (nf) {
+    st.failed[p] = it;
+    st.stop_iter[p] = it;
+    return 0;
+  }
+  const double norm = sqrt(s);
+  st.norms[size_t(it - 1) * P + p] = norm;
+  st.iters[p] = it;
+  const double prev = st.prev_norm[p];
+  int run = 0;
+  if (it >= 2 && fabs(norm - prev) / fmax(prev, 1e-30) <= rel_tol) {
+    st.converged[p] = 1;
+    st.stop_iter[p] = it;
+  } else if (it >= max_iters) {
+    st.stop_iter[p] = it;
+  } else {
+    run = 1;
+  }
+  st.prev_norm[p] = norm;
+  return run;
+}
+
 // Reduce iteration `it` for every still-running plane and apply the stop
-// rule of fixed_point_solve (solver.py:347-358).  Executed by ONE warp:
-// lane-per-plane, each lane sums its plane's partials sequentially in a
-// fixed order, so the norms are bitwise reproducible.
+// rule.  Executed by ONE warp, always in a fixed order so the norms are
+// bitwise reproducible: planes with many partials are reduced warp-wide
+// (lane-strided loads in flight together, fixed xor tree); planes with few
+// partials (batches) lane-per-plane.
 __device__ __forceinline__ void finalize_iteration_warp(const StateView& st, const Partials& pt,
                                                         int P, int it, int max_iters,
                                                         double rel_tol) {
   const int lane = threadIdx.x & 31;
   int running = 0;
+  if (pt.nbmax > 8) {
+    for (int p = 0; p < P; ++p) {
+      if (st.stop_iter[p] != 0) continue;
+      const size_t base = (size_t(it % pt.ring) * P + p) * pt.nbmax;
+      const int n = partial_count(pt, p);
+      double s = 0.0;
+      int nf = 0;
+      for (int b = lane; b < n; b += 32) {
+        s += pt.sum[base + b];
+        nf |= pt.flag[base + b];
+      }
+      s = warp_sum(s);
+      nf = __any_sync(0xffffffffu, nf);
+      if (lane == 0) running += finalize_plane(st, P, p, it, max_iters, rel_tol, s, nf);
+    }
+    if (lane == 0) st.running[0] = running;
+    return;
+  }
   for (int p = lane; p < P; p += 32) {
     if (st.stop_iter[p] != 0) continue;
     const size_t base = (size_t(it % pt.ring) * P + p) * pt.nbmax;
@@ -72,24 +119,7 @@ __device__ __forceinline__ void finalize_iteration_warp(const StateView& st, con
       s += pt.sum[base + b];
       nf |= pt.flag[base + b];
     }
-    if (nf) {
-      st.failed[p] = it;
-      st.stop_iter[p] = it;
-      continue;
-    }
-    const double norm = sqrt(s);
-    st.norms[size_t(it - 1) * P + p] = norm;
-    st.iters[p] = it;
-    const double prev = st.prev_norm[p];
-    if (it >= 2 && fabs(norm - prev) / fmax(prev, 1e-30) <= rel_tol) {
-      st.converged[p] = 1;
-      st.stop_iter[p] = it;
-    } else if (it >= max_iters) {
-      st.stop_iter[p] = it;
-    } else {
-      ++running;
-    }
-    st.prev_norm[p] = norm;
+    running += finalize_plane(st, P, p, it, max_iters, rel_tol, s, nf);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) running += __shfl_xor_sync(0xffffffffu, running, o);

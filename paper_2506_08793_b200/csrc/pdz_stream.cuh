@@ -2,38 +2,48 @@
 //
 // Same mathematics as the tiled sweep (pdz_sweep.cu; solver.py:280-302), laid
 // out for B200:
-//  * ONE cooperative launch runs all sweeps of a solve.  CTA i owns the same
-//    exactly balanced range [floor(iS/G), floor((i+1)S/G)) of the S = planes x
-//    strips x H "strip-rows" (strip = 64 output columns) in every sweep, so
-//    every SM gets the same pixels (+-1 row) -- no wave quantisation on 148
-//    SMs, no per-sweep launch, no grid-wide barrier: before sweep n a CTA only
-//    waits (acquire loads of per-CTA progress counters) for the CTAs whose
-//    rows its stencil reads -- its strip and the two neighbouring strips,
-//    +-R rows -- to have published sweep n-1.  The same wait protects the
-//    ping-pong buffer it overwrites (those CTAs were its readers).
-//  * inside a sweep the CTA streams down its range in blocks of 32 rows:
-//    input rows (64 + 2*ceil4(R) columns) arrive by cp.async.bulk (TMA bulk
-//    copies, UBLKCP) into a double buffer signalled by an mbarrier while the
-//    previous block computes; horizontally blurred rows of the 2R-row overlap
-//    are carried between blocks (only range/strip starts pay the halo);
+//  * ONE cooperative launch runs the whole solve, one CTA per SM (15 compute
+//    warps + 1 service warp).  The S = images x strips x H "strip-rows"
+//    (strip = 64 output columns of one image) are split into G exactly
+//    balanced ranges [floor(iS/G), floor((i+1)S/G)), aligned to strips; CTA i
+//    owns range i for EVERY channel of those images, so every SM gets the
+//    same pixels (+-1 row): no wave quantisation, no per-sweep launch and no
+//    grid-wide barrier.
+//  * a CTA walks one flat stream of blocks ordered (iteration n, channel c,
+//    block of <= 120 rows; config 2 has one block per pass).  Pass (n, c)
+//    reads channel c of iterate n-1, so it only
+//    waits until the CTAs whose rows its stencil reads (its strip and the
+//    neighbouring strips, +-R rows) have published pass (n-1, c) -- done
+//    C - 1 passes earlier, so in steady state nobody waits.  A per-CTA
+//    progress counter (passes completed) carries that ordering (release /
+//    acquire); the same wait protects the ping-pong buffer being overwritten.
+//  * the two iterate buffers are PADDED, [P][H + 2R][W + 2 ceil4(R)]: the
+//    producer of an output near an image border also stores its mirrored
+//    copies into the pads (np.pad "symmetric", solver.py:235), so no reader
+//    ever reflects an index.  Each block's input rows (64 + 2 ceil4(R)
+//    columns) arrive by ONE TMA tile load (cp.async.bulk.tensor, UTMALDG)
+//    into a double buffer, signalled by an mbarrier and always queued one
+//    block ahead -- across pass boundaries too.
 //  * horizontal Gaussian from shared memory (8 outputs per item), vertical
 //    pass with packed FFMA2 over column pairs, MUFU sqrt/rcp face fluxes,
-//    residual, update and r^2 fused in registers;
-//  * warps 0-3 compute; warp 4 of CTA 0 is the service warp: it waits for
-//    every CTA to publish sweep m, reduces the r^2 partials of m in a fixed
-//    order (bitwise reproducible), applies the stop rule (solver.py:347-358)
-//    and publishes `fin = m`.  Partials live in a ring of kRing slots; a CTA
-//    writing slot n % kRing first waits for fin >= n - kRing, and with the
-//    stop rule active it waits for fin >= n - 2 so planes stopped at <= n-2
-//    are skipped (their answer stays in buf[stop & 1]).
-// Border handling: rows are reflected (np.pad "symmetric", solver.py:235) at
-// load time; out-of-image columns are fixed up in shared memory from their
-// reflected in-window sources; the centred differences use the one-sided
-// form at the first/last row/column (np.gradient, solver.py:178-179).
-// Requirements: width % 4 == 0 (16-byte bulk copies), a compiled radius, and
-// all G CTAs co-resident (cooperative launch); otherwise the tiled kernel.
+//    residual, update and r^2 fused in registers.
+//  * warps 0-14 compute; warp 15 (service) does every gpu-scope
+//    synchronisation: it releases the CTA's pass counter to global memory
+//    and grants the compute warps the passes whose inputs are published, so
+//    compute warps never execute a gpu-scope fence.
+//  * one extra CTA finalises sweep n once every CTA published it: it reduces
+//    the r^2 partials in a fixed order (bitwise reproducible), applies the
+//    stop rule (solver.py:347-358) and releases `fin = n`.  Partials live in
+//    a ring of kRing iteration slots: pass (n, c) waits for fin >= n - kRing,
+//    and with the stop rule for fin >= n - 2 so planes stopped at <= n-2 are
+//    skipped (their answer stays in buf[stop & 1]).
+// Requirements: width % 4 == 0 (TMA strides), H >= 2R and W >= 2 ceil4(R)
+// (one reflection fold), a compiled radius, and all G + 1 CTAs co-resident
+// (cooperative launch; G + 1 <= SMs); otherwise the tiled kernel is used.
 // Every spin has a 10 s timeout that sets an abort flag instead of hanging.
 #pragma once
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -42,8 +52,8 @@
 namespace pdz {
 
 constexpr int kSTW = 64;                    // strip width (output columns)
-constexpr int kSRB = 32;                    // output rows per block (4 warps x 8)
-constexpr int kSCW = 4;                     // compute warps
+constexpr int kSCW = 15;                    // compute warps
+constexpr int kSRB = kSCW * 8;              // output rows per block (8 per warp)
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
@@ -51,32 +61,50 @@ constexpr long long kSpinTimeoutNs = 10000000000ll;
 
 template <int R>
 struct SGeo {
-  static constexpr int RP = (R + 3) & ~3;  // column halo rounded to float4
-  static constexpr int PWD = kSTW + 2 * RP;  // staged floats per row
-  static constexpr int PITCH = PWD;          // 16-byte aligned smem rows
-  static constexpr int ROWS = kSRB + 2 * R;  // staged input rows / H rows
-  static constexpr int IN_FLOATS = ROWS * PITCH;
-  static constexpr int H_FLOATS = ROWS * kSTW;
-  static constexpr size_t SMEM = size_t(2 * IN_FLOATS + 2 * H_FLOATS) * 4 + 128;
+  static constexpr int RP = (R + 3) & ~3;      // column halo rounded to float4
+  static constexpr int PITCH = kSTW + 2 * RP;  // staged floats per row = TMA box width
+  static constexpr int ROWS = kSRB + 2 * R;    // staged input rows / H rows = TMA box height
+  static constexpr int IN_FLOATS = (ROWS * PITCH + 31) & ~31;  // 128-byte aligned buffers
+  static constexpr int H_FLOATS = (ROWS * kSTW + 31) & ~31;
+  static constexpr size_t SMEM = size_t(2 * IN_FLOATS + H_FLOATS) * 4 + 128;
 };
 
 struct StreamArgs {
+  // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2RP], box
+  // {PITCH, kSRB + 2R, 1}.
+  CUtensorMap tm[2];
   float* buf0;
   float* buf1;
   const float* phi;
   const float* lam;
   Partials pt;          // ring of kRing slots
-  StateView st;         // st.stop_iter == nullptr: single step (no service warp)
-  int32_t* done;        // [G] last sweep each CTA has published
-  int32_t* fin;         // [1] last iteration the service warp finalised
-  int32_t* flags;       // [0] every plane stopped, [1] abort (spin timeout)
+  StateView st;         // st.stop_iter == nullptr: single step (no finalisation)
+  int32_t* done;        // [G] passes published by each CTA
+  int32_t* fin;         // [1] last iteration finalised
+  int32_t* flags;       // [0] iteration by which every plane stopped, [1] abort
   int32_t H, W, P, C, nstrips;
-  int32_t iter_first, iter_last, max_iters;
-  int32_t stop_rule;    // rel_tol active: sweep n needs fin >= n - 2
+  int32_t iter_last, max_iters;  // sweeps 1..iter_last
+  int32_t stop_rule;    // rel_tol active: pass (n, c) needs fin >= n - 2
   float eps, tau;
   double rel_tol;
+  long long* prof;      // -DPDZ_PROFILE builds + PDZ_PROF=1: [2G+1][16] wait times
   float w[kMaxTaps];
 };
+
+// Profiling instrumentation (tools/prof_stream.py): compiled only with
+// -DPDZ_PROFILE (build with PDZ_PROFILE=1), absent from the product build.
+#ifdef PDZ_PROFILE
+#define PDZ_P(...) __VA_ARGS__
+#define PDZ_PT(slot, stmt)            \
+  {                                   \
+    const long long t_ = global_ns(); \
+    stmt;                             \
+    pf[slot] += global_ns() - t_;     \
+  }
+#else
+#define PDZ_P(...)
+#define PDZ_PT(slot, stmt) stmt
+#endif
 
 // ------------------------------------------------------------ primitives --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -113,28 +141,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// Order this thread's earlier generic-proxy global accesses (as observed via
-// the acquire) before its later async-proxy (bulk copy) accesses.
+// 3-D tile load (TMA): box at (x, y, z) -> dst, completion counted on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// Order this thread's generic-proxy view (after an acquire) before its later
+// async-proxy (TMA) reads of global memory.
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ int ld_acquire(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// Polling load: relaxed (no L1 invalidation per poll); the caller issues one
-// acquire fence once the condition holds.
+// Polling load: relaxed (no L1 invalidation per poll); one acquire fence
+// follows once the condition holds.
 __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void fence_acquire_gpu() {
+__device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_shared(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ long long global_ns() {
   long long t;
@@ -172,35 +212,44 @@ __device__ __forceinline__ float sflux(float jump, float along, float eps) {
   return jump * rcp_approx(sqrt_approx(s) + eps);
 }
 
+// ----------------------------------------------------------- iteration --
 struct SBlock {
-  int p, x0, yb, n, first;
+  int p, x0, yb, n;         // plane, strip origin, first row, rows
+  int iter, c, pass_start;  // pass (iter, c); first block of the pass
 };
 
-// Walks a CTA's range [L0, L1) of strip-rows block by block: (plane p, strip
-// s, row y) advance incrementally, so only the start needs divisions.  Planes
-// frozen at <= iter-2 are skipped.  (32-bit: the host only selects this
-// kernel when S < 2^31.)
+// One pass over the CTA's range [L0, L1) of strip-rows: (image b, strip s,
+// row y) advance incrementally.  Planes frozen at <= iter-2 are skipped.
 struct RangeIter {
-  int L, L0, L1, p, s, y;
+  int L, L0, L1, b, s, y;
+  int b0, s0, y0;
   __device__ __forceinline__ void init(int l0, int l1, const StreamArgs& a) {
     L = L0 = l0;
     L1 = l1;
     const int u = l0 / a.H;
-    y = l0 - u * a.H;
-    p = u / a.nstrips;
-    s = u - p * a.nstrips;
+    y0 = l0 - u * a.H;
+    b0 = u / a.nstrips;
+    s0 = u - b0 * a.nstrips;
+    reset();
+  }
+  __device__ __forceinline__ void reset() {
+    L = L0;
+    b = b0;
+    s = s0;
+    y = y0;
   }
   __device__ __forceinline__ void wrap(const StreamArgs& a) {
     y = 0;
     if (++s == a.nstrips) {
       s = 0;
-      ++p;
+      ++b;
     }
   }
-  __device__ __forceinline__ bool next(const StreamArgs& a, int iter, SBlock& b) {
+  __device__ __forceinline__ bool next(const StreamArgs& a, int iter, int c, SBlock& blk) {
     while (L < L1) {
       const int seg_end = min(L1, L - y + a.H);
-      if (a.st.stop_iter) {
+      const int p = b * a.C + c;
+      if (a.stop_rule && a.st.stop_iter) {
         const int st = a.st.stop_iter[p];
         if (st != 0 && st < iter - 1) {
           L = seg_end;
@@ -208,13 +257,12 @@ struct RangeIter {
           continue;
         }
       }
-      b.p = p;
-      b.x0 = s * kSTW;
-      b.yb = y;
-      b.n = min(kSRB, seg_end - L);
-      b.first = (L == L0) || (y == 0);
-      L += b.n;
-      y += b.n;
+      blk.p = p;
+      blk.x0 = s * kSTW;
+      blk.yb = y;
+      blk.n = min(kSRB, seg_end - L);
+      L += blk.n;
+      y += blk.n;
       if (y == a.H) wrap(a);
       return true;
     }
@@ -222,123 +270,335 @@ struct RangeIter {
   }
 };
 
-// Warp 0 of the compute warps: queue the bulk copies of the block's new input
-// rows (reflected row indices, in-image column span) into `in`.
+// Progress counter value once pass (n, c) is complete.
+__device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter - 1) * C + c + 1; }
+
+enum { kEnd = 0, kBlock = 1, kDefer = 2 };
+constexpr int kNoMirror = -0x40000000;
+constexpr int kGrantAll = 0x7fffffff;
+
+// Compute threads: wait until the service warp has granted pass k (shared
+// memory, CTA scope -- no gpu-scope fence on the compute path).
+__device__ __forceinline__ void wait_grant(const int* s_grant, int k) {
+  while (ld_acquire_cta_shared(s_grant) < k) __nanosleep(20);
+}
+
+// Flat stream of (iteration, channel, block).  Passes with no blocks (every
+// plane of the range frozen) are skipped.  `busy` = progress index of the
+// pass of a block still in flight (0: none).  A pass whose grant depends on
+// that pass's completion (its neighbour wait covers this CTA's own pass
+// (n-1, c)) is deferred until the CTA is idle, so a CTA never waits on
+// itself.  When idle, skipped passes are published at once.
+struct FlatIter {
+  RangeIter r;
+  int iter, c;
+  bool fresh;  // next block starts a new pass
+  bool ended;
+  PDZ_P(long long grant_ns;)
+  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy,
+                                      int* s_progress, const int* s_grant) {
+    while (!ended && iter <= a.iter_last) {
+      if (fresh) {
+        if (busy && iter >= 2 && pass_index(iter - 1, c, a.C) >= busy) return kDefer;
+        PDZ_P(const long long tg = global_ns();)
+        wait_grant(s_grant, pass_index(iter, c, a.C));
+        PDZ_P(grant_ns += global_ns() - tg;)
+        if (a.stop_rule && a.st.stop_iter) {
+          // granted => fin >= iter - 2 (or every plane had stopped); the
+          // all-stopped iteration is published before fin reaches it, so
+          // this test is uniform across threads
+          const int all = ld_relaxed(a.flags);
+          if (all != 0 && all <= iter - 2) {
+            ended = true;
+            break;
+          }
+        }
+      }
+      if (r.next(a, iter, c, blk)) {
+        blk.iter = iter;
+        blk.c = c;
+        blk.pass_start = fresh;
+        fresh = false;
+        return kBlock;
+      }
+      if (!busy && threadIdx.x == 0) st_release_cta_shared(s_progress, pass_index(iter, c, a.C));
+      if (++c == a.C) {
+        c = 0;
+        ++iter;
+      }
+      r.reset();
+      fresh = true;
+    }
+    ended = true;
+    return kEnd;
+  }
+  // Progress index of the last pass before the iterator position.
+  __device__ __forceinline__ int completed(const StreamArgs& a) const {
+    return ended ? pass_index(a.iter_last, a.C - 1, a.C) : pass_index(iter, c, a.C) - 1;
+  }
+};
+
+// ----------------------------------------------------------- row loads --
+// Warp 0: queue a block's new input rows with ONE TMA tile load.  The iterate
+// buffers are padded ([P][H + 2R][W + 2RP], the pads holding the symmetric
+// reflection written by the producers), so every needed row and column --
+// image borders included -- is a plain box of the padded tensor.
+// Staged row i holds image row yb - R + i (padded row yb + i); rows beyond the
+// block's n + 2R are over-fetch, never read.
 template <int R>
-__device__ __forceinline__ void issue_rows(const SBlock& b, const float* __restrict__ uin,
-                                           float* in, uint64_t* bar, int H, int W, int lane) {
+__device__ __forceinline__ void issue_block(const StreamArgs& a, const SBlock& b,
+                                            float* in, uint64_t* bar, int lane) {
   using Gm = SGeo<R>;
-  const int r0 = b.first ? b.yb - R : b.yb + R;
-  const int nrows = b.first ? b.n + 2 * R : b.n;
-  const int idx0 = b.first ? 0 : R + 1;
-  const int gc0 = max(0, b.x0 - Gm::RP);
-  const int gc1 = min(W, b.x0 + kSTW + Gm::RP);
-  const uint32_t bytes = uint32_t(gc1 - gc0) * 4u;
-  if (lane == 0) mbar_expect_tx(bar, bytes * uint32_t(nrows));
+  const int buf = (b.iter - 1) & 1;  // the buffer pass `iter` reads
+  if (lane == 0) {
+    mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
+    tma_load_3d(in, &a.tm[buf], b.x0, b.yb, b.p, bar);
+  }
   __syncwarp();
-  const int dcol = gc0 - (b.x0 - Gm::RP);
-  for (int i = lane; i < nrows; i += 32) {
-    const int gy = reflect(r0 + i, H);
-    bulk_g2s(in + (idx0 + i) * Gm::PITCH + dcol, uin + size_t(gy) * W + gc0, bytes, bar);
-  }
 }
 
-// One warp: spin until done[lo..hi] >= need and the fin conditions hold.
-// Returns false on stop-all or abort (timeout).
-__device__ bool wait_deps(const StreamArgs& a, int lo, int hi, int need_done, int need_fin) {
+// --------------------------------------------------------- service warp --
+// CTAs whose output rows a CTA's stencil reads: up to 3 intervals of CTA
+// indices (the strips left / right and its own strip, rows +-R); a range that
+// spans several strips uses one covering interval.
+struct DepSet {
+  int lo[3], hi[3], n;  // three intervals (hi < lo: empty)
+};
+__device__ __forceinline__ DepSet dep_set(const StreamArgs& a, int L0, int L1, int R) {
+  DepSet d;
+  const int S = int(a.pt.S), G = a.pt.G, H = a.H;
+  const int u0 = L0 / H, u1 = (L1 - 1) / H;
+  if (u0 != u1) {
+    d.n = 3;
+    d.lo[0] = int(cta_of(max(0, L0 - H - R), S, G));
+    d.hi[0] = int(cta_of(min(S - 1, L1 - 1 + H + R), S, G));
+    d.lo[1] = d.lo[2] = 1;
+    d.hi[1] = d.hi[2] = 0;
+    return d;
+  }
+  const int b = u0 / a.nstrips, s = u0 - b * a.nstrips;
+  const int y0 = max(0, L0 - u0 * H - R), y1 = min(H, L1 - u0 * H + R);
+  d.n = 3;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {  // strips s-1, s, s+1 (empty interval if absent)
+    const int s2 = s + i - 1;
+    const int base = (b * a.nstrips + s2) * H;
+    const bool ok = s2 >= 0 && s2 < a.nstrips;
+    d.lo[i] = ok ? int(cta_of(base + y0, S, G)) : 1;
+    d.hi[i] = ok ? int(cta_of(base + y1 - 1, S, G)) : 0;
+  }
+  return d;
+}
+
+__device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Warp kSCW runs every gpu-scope synchronisation of its CTA, so compute warps
+// never execute a gpu-scope fence (which would wait for their in-flight
+// output stores).  One fence per round serves both directions:
+//  * publish: the compute warps' completed-pass counter (shared memory,
+//    written after a CTA barrier) is released to done[cta];
+//  * grant: pass k = (n, c) may start once the CTAs whose rows it reads have
+//    published pass (n-1, c), partial slot n % kRing is free (fin >= n -
+//    kRing) and, with the stop rule, fin >= n - 2; granted passes are
+//    released to the compute warps through shared memory, up to 3 passes
+//    beyond the published counter.  Once every plane has stopped everything
+//    is granted (the compute warps then end).
+__device__ void service_loop(const StreamArgs& a, const int* s_progress, const int* s_exit,
+                             int* s_grant, const DepSet& dep) {
   const int lane = threadIdx.x & 31;
-  const long long t0 = global_ns();
-  unsigned ns = 32;
+  const int C = a.C;
+  const bool fin_on = a.st.stop_iter != nullptr;
+  const int total = pass_index(a.iter_last, C - 1, C);
+  int published = 0;
+  int granted = 0;
+  long long t0 = global_ns();
+  PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
+  PDZ_P(long long t_need = 0;)
   while (true) {
-    bool ok = true;
-    for (int j = lo + lane; j <= hi; j += 32) ok &= ld_relaxed(a.done + j) >= need_done;
-    if (lane == 0 && need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
-    ok = __all_sync(0xffffffffu, ok);
-    const int stop = ld_relaxed(a.flags) | ld_relaxed(a.flags + 1);
-    if (__any_sync(0xffffffffu, stop != 0)) return false;
-    if (ok) {
-      fence_acquire_gpu();
-      return true;
+    const bool last = ld_acquire_cta_shared(s_exit) != 0;  // before the counter:
+    const int x = ld_acquire_cta_shared(s_progress);       // it is final once `last`
+    const bool pub = x > published;
+    bool grant = false, all_stopped = false;
+    if (granted < total && granted < x + 3) {
+      const int k = granted + 1;
+      PDZ_P(if (t_need == 0) t_need = global_ns();)
+      const int n = (k - 1) / C + 1;
+      bool ok = true;
+      if (n >= 2) {
+        const int need = k - C;  // pass (n-1, c)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
+            ok &= ld_relaxed(a.done + j) >= need;
+      }
+      if (lane == 0 && fin_on) {
+        const int need_fin = a.stop_rule ? n - 2 : n - kRing;
+        if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
+      }
+      grant = __all_sync(0xffffffffu, ok);
+      if (!grant && fin_on && a.stop_rule) all_stopped = ld_relaxed(a.flags) != 0;
     }
-    if (global_ns() - t0 > kSpinTimeoutNs) {
-      if (lane == 0) atomicExch(a.flags + 1, 1);
-      return false;
+    if (pub || grant || all_stopped) {
+      PDZ_P(const long long tf_ = global_ns();)
+      fence_acq_rel_gpu();  // release for the publication, acquire for the grant
+      PDZ_P(sp[0] += global_ns() - tf_; sp[1] += 1;)
+      if (pub) {
+        if (lane == 0) st_relaxed(a.done + blockIdx.x, x);
+        published = x;
+      }
+      if (grant || all_stopped) {
+        granted = all_stopped ? total : granted + 1;
+        if (lane == 0) st_release_cta_shared(s_grant, all_stopped ? kGrantAll : granted);
+        PDZ_P(sp[4] += global_ns() - t_need; sp[5] += 1; t_need = 0;)
+      }
+      t0 = global_ns();
+      continue;
     }
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
+    if (last) {
+      PDZ_P(if (a.prof && lane == 0) for (int i = 0; i < 8; ++i)
+                a.prof[(a.pt.G + 1 + blockIdx.x) * 16 + i] = sp[i];)
+      return;
+    }
+    if (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs) {
+      if (lane == 0) {
+        atomicExch(a.flags + 1, 1);
+        st_release_cta_shared(s_grant, kGrantAll);
+      }
+      return;
+    }
+    __nanosleep(64);
   }
 }
 
-// CTA 0 / warp kSCW: finalise iterations as soon as every CTA published them.
-__device__ void service_loop(const StreamArgs& a) {
-  const int lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  for (int m = a.iter_first; m <= a.iter_last; ++m) {
+// ------------------------------------------------------------ finaliser --
+// The extra CTA (index G) finalises sweeps in order: once every compute CTA
+// has published sweep n, it reduces sweep n's r^2 partials in a fixed order
+// (bitwise reproducible), applies the stop rule (solver.py:347-358) and
+// releases fin = n; it ends when every plane has stopped.
+__device__ void finalizer_cta(const StreamArgs& a) {
+  if (!a.st.stop_iter) return;
+  __shared__ int s_run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kSThreads / 32;
+  const int G = a.pt.G, C = a.C, P = a.P;
+  const Partials& pt = a.pt;
+  for (int n = 1; n <= a.iter_last; ++n) {
+    const int need = pass_index(n, C - 1, C);
     const long long t0 = global_ns();
-    unsigned ns = 64;
     while (true) {
       bool ok = true;
-      for (int j = lane; j < G; j += 32) ok &= ld_relaxed(a.done + j) >= m;
-      ok = __all_sync(0xffffffffu, ok);
-      if (ok) {
-        fence_acquire_gpu();
-        break;
-      }
-      if (__any_sync(0xffffffffu, ld_relaxed(a.flags + 1) != 0)) return;
-      if (global_ns() - t0 > kSpinTimeoutNs) {
-        if (lane == 0) atomicExch(a.flags + 1, 1);
+      for (int i = tid; i < G; i += kSThreads) ok &= ld_relaxed(a.done + i) >= need;
+      if (__syncthreads_and(ok)) break;
+      const bool bad = ld_relaxed(a.flags + 1) != 0 || global_ns() - t0 > kSpinTimeoutNs;
+      if (__syncthreads_or(bad)) {
+        if (tid == 0) atomicExch(a.flags + 1, 1);
         return;
       }
-      __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
+      __nanosleep(100);
     }
-    finalize_iteration_warp(a.st, a.pt, a.P, m, a.max_iters, a.rel_tol);
-    __syncwarp();
-    __threadfence();
-    const int running = a.st.running[0];
-    if (lane == 0) {
-      if (running == 0) atomicExch(a.flags, 1);
-      st_release(a.fin, m);
+    fence_acq_rel_gpu();
+    if (tid == 0) s_run = 0;
+    __syncthreads();
+    int running = 0;
+    if (pt.nbmax <= 32) {  // many planes, few partials each: thread per plane
+      for (int p = tid; p < P; p += kSThreads) {
+        if (a.st.stop_iter[p] != 0) continue;
+        const size_t base = (size_t(n % pt.ring) * P + p) * pt.nbmax;
+        const int cnt = partial_count(pt, p);
+        double s = 0.0;
+        int nf = 0;
+#pragma unroll 8
+        for (int b = 0; b < cnt; ++b) {
+          s += pt.sum[base + b];
+          nf |= pt.flag[base + b];
+        }
+        running += finalize_plane(a.st, P, p, n, a.max_iters, a.rel_tol, s, nf);
+      }
+    } else {  // few planes, many partials: warp per plane, lane-strided
+      for (int p = warp; p < P; p += NW) {
+        if (a.st.stop_iter[p] != 0) continue;
+        const size_t base = (size_t(n % pt.ring) * P + p) * pt.nbmax;
+        const int cnt = partial_count(pt, p);
+        double s = 0.0;
+        int nf = 0;
+#pragma unroll 8
+        for (int b = lane; b < cnt; b += 32) {
+          s += pt.sum[base + b];
+          nf |= pt.flag[base + b];
+        }
+        s = warp_sum(s);
+        nf = __any_sync(0xffffffffu, nf);
+        if (lane == 0) running += finalize_plane(a.st, P, p, n, a.max_iters, a.rel_tol, s, nf);
+      }
     }
-    if (running == 0) return;
+    if (running) atomicAdd(&s_run, running);
+    __syncthreads();
+    const int run = s_run;
+    if (tid == 0) {
+      a.st.running[0] = run;
+      if (run == 0) a.flags[0] = n;
+      fence_acq_rel_gpu();
+      st_relaxed(a.fin, n);
+    }
+    if (run == 0) return;
+    __syncthreads();  // s_run is reset next round
   }
 }
 
+// ------------------------------------------------------------- kernel --
 template <int R, bool EDGE>
-__global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a) {
+__global__ void __launch_bounds__(kSThreads, 1)
+    stream_kernel(const __grid_constant__ StreamArgs a) {
   using Gm = SGeo<R>;
   extern __shared__ __align__(128) float smem[];
   float* const in0 = smem;
   float* const in1 = smem + Gm::IN_FLOATS;
-  float* const h0 = smem + 2 * Gm::IN_FLOATS;
-  float* const h1 = h0 + Gm::H_FLOATS;
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(h1 + Gm::H_FLOATS);
+  float* const hbuf = smem + 2 * Gm::IN_FLOATS;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(hbuf + Gm::H_FLOATS);
   __shared__ double s_red[kSCW];
   __shared__ int s_nf[kSCW];
-  __shared__ int s_go;
+  __shared__ int s_progress, s_exit, s_grant;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_fence_init();
+    s_progress = 0;
+    s_exit = 0;
+    s_grant = 0;
   }
   __syncthreads();
 
-  if (warp == kSCW) {  // service warp
-    if (a.st.stop_iter && blockIdx.x == 0) service_loop(a);
-    return;
-  }
-
   const int H = a.H, W = a.W;
-  const size_t plane = size_t(H) * W;
+  const size_t plane = size_t(H) * W;                    // Phi / lambda planes (dense)
+  constexpr int RP = Gm::RP;
+  const int WP = W + 2 * RP;                             // padded iterate row
+  const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
   const int S = int(a.pt.S), G = a.pt.G;
   const int L0 = int(cta_start(blockIdx.x, S, G));
   const int L1 = int(cta_start(blockIdx.x + 1, S, G));
-  // CTAs whose output rows this CTA's stencil reads: same strip +-R rows and
-  // the neighbouring strips (a superset: one interval of the linear order).
-  const int dep_lo = int(cta_of(max(0, L0 - H - R), S, G));
-  const int dep_hi = int(cta_of(min(S - 1, L1 - 1 + H + R), S, G));
+  if (blockIdx.x == a.pt.G) {  // the extra CTA: finaliser
+    finalizer_cta(a);
+    return;
+  }
+  if (warp == kSCW) {
+    service_loop(a, &s_progress, &s_exit, &s_grant, dep_set(a, L0, L1, R));
+    return;
+  }
+
+  FlatIter it;
+  it.r.init(L0, L1, a);
+  it.iter = 1;  // pass numbering (done[], grants) starts at sweep 1
+  it.c = 0;
+  it.fresh = true;
+  it.ended = false;
+  PDZ_P(it.grant_ns = 0;)
+  PDZ_P(long long pf[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};)
+  PDZ_P(long long tph = 0;)
+  PDZ_P(const long long tk0 = global_ns();)
 
   // thread roles for the vertical pass / update: column pair, 8-row group
   const int c = 2 * lane;   // strip-local output column of the pair
@@ -346,273 +606,251 @@ __global__ void __launch_bounds__(kSThreads, 3) stream_kernel(const StreamArgs a
   uint32_t phase0 = 0, phase1 = 0;
   int ib = 0;
 
-  for (int iter = a.iter_first; iter <= a.iter_last; ++iter) {
-    // ---- dependencies: neighbours published iter-1; ring slot / stop state
-    if (warp == 0) {
-      int need_fin = iter - kRing;
-      if (a.stop_rule) need_fin = max(need_fin, iter - 2);
-      const bool go = wait_deps(a, dep_lo, dep_hi, iter - 1, a.st.stop_iter ? need_fin : 0);
-      if (lane == 0) s_go = go ? 1 : 0;
-      fence_proxy_async_global();
+  SBlock cur, nxt;
+  bool have = it.next(a, cur, 0, &s_progress, &s_grant) == kBlock;
+  if (have && warp == 0) {
+    fence_proxy_async_global();
+    issue_block<R>(a, cur, in0, &bars[0], lane);
+  }
+  double acc_r2 = 0.0;
+  float acc_nf = 0.0f;
+
+  // Per block b (two CTA barriers):
+  //   barrier (block b-1 finished: IN(b-1) and H are free)
+  //   -> queue IN(b+1) (overlaps all of block b; granted first when b+1
+  //      starts a pass)
+  //   -> wait IN(b); blur its n + 2R rows into H
+  //   -> barrier
+  //   -> vertical pass + divergence + update.
+  while (have) {
+    PDZ_P(const long long tn_ = global_ns();)
+    const int nk = it.next(a, nxt, pass_index(cur.iter, cur.c, a.C), &s_progress, &s_grant);
+    PDZ_P(pf[12] += global_ns() - tn_;)
+    bool have_nxt = nk == kBlock;
+    float* const in_cur = ib ? in1 : in0;
+    float* const in_nxt = ib ? in0 : in1;
+    float* const h_cur = hbuf;
+    uint64_t* const bar_cur = &bars[ib];
+    uint64_t* const bar_nxt = &bars[ib ^ 1];
+    const int gx = cur.x0 + c;
+    const bool col_ok = gx < W;
+    float* __restrict__ uout_all = (cur.iter & 1) ? a.buf1 : a.buf0;
+
+    PDZ_PT(2, compute_bar());
+    PDZ_P(pf[6] += 1;)
+    if (have_nxt && warp == 0) {
+      if (nxt.pass_start) fence_proxy_async_global();  // granted data -> TMA reads
+      issue_block<R>(a, nxt, in_nxt, bar_nxt, lane);
     }
-    compute_bar();
-    if (!s_go) return;
 
-    const float* __restrict__ uin_all = ((iter - 1) & 1) ? a.buf1 : a.buf0;
-    float* __restrict__ uout_all = (iter & 1) ? a.buf1 : a.buf0;
-    RangeIter it;
-    it.init(L0, L1, a);
-    SBlock cur, nxt;
-    bool have = it.next(a, iter, cur);
-    if (have && warp == 0)
-      issue_rows<R>(cur, uin_all + cur.p * plane, ib ? in1 : in0, &bars[ib], H, W, lane);
-    double acc_r2 = 0.0;
-    float acc_nf = 0.0f;
-    int acc_p = have ? cur.p : -1;
+    PDZ_P(tph = global_ns();)
+    // ---- prefetch Phi / lambda for this thread's outputs into registers
+    float2 phv[8], lmv[8];
+    {
+      const size_t off0 = size_t(cur.yb + j0) * W + gx;
+      const float2* __restrict__ ph =
+          reinterpret_cast<const float2*>(a.phi + cur.p * plane + off0);
+      const float2* __restrict__ lm =
+          reinterpret_cast<const float2*>(a.lam + (cur.p / a.C) * plane + off0);
+      const int rows_here = col_ok ? min(8, cur.n - j0) : 0;
+      const int w2 = W >> 1;  // row stride in float2
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < rows_here) {
+          phv[j] = __ldg(ph + j * w2);
+          lmv[j] = __ldg(lm + j * w2);
+        } else {
+          phv[j] = make_float2(0.f, 0.f);
+          lmv[j] = make_float2(0.f, 0.f);
+        }
+      }
+    }
 
-    // One CTA barrier per block:
-    //   wait IN(b) [+ border fix-up + barrier, border strips only]
-    //   -> carry H overlap, blur the new rows into H(b)
-    //   -> barrier
-    //   -> carry the IN overlap into the other buffer, queue IN(b+1),
-    //      vertical pass + divergence + update of block b.
-    // H(b) is written while only H(b-1) is read; IN(b+1) overwrites the
-    // buffer last read by block b-1, which every thread finished before the
-    // barrier.
-    while (have) {
-      const bool have_nxt = it.next(a, iter, nxt);
-      float* const in_cur = ib ? in1 : in0;
-      float* const in_nxt = ib ? in0 : in1;
-      float* const h_cur = ib ? h1 : h0;
-      float* const h_prev = ib ? h0 : h1;
-      uint64_t* const bar_cur = &bars[ib];
-      uint64_t* const bar_nxt = &bars[ib ^ 1];
-      const int gx = cur.x0 + c;
-      const bool col_ok = gx < W;
+    // ---- wait for this block's input rows
+    if (ib) {
+      PDZ_PT(3, mbar_wait(bar_cur, phase1));
+      phase1 ^= 1;
+    } else {
+      PDZ_PT(3, mbar_wait(bar_cur, phase0));
+      phase0 ^= 1;
+    }
+    PDZ_P(pf[11] += global_ns() - tph; tph = global_ns();)
+    // ---- H rows: horizontal blur of the n + 2R staged rows
+    // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R)
+    // staged values per 8 outputs.
+    const int hn = cur.n + 2 * R;
+    for (int item = tid; item < hn * (kSTW / 8); item += kComputeThreads) {
+      const int i = item >> 3, g = item & 7;
+      const float* row = in_cur + i * Gm::PITCH + 8 * g;
+      constexpr int OFF = Gm::RP - R;
+      constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
+      float v[4 * NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 t = reinterpret_cast<const float4*>(row)[q];
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+      }
+      float o[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) o[m] = 0.f;
+#pragma unroll
+      for (int k = 0; k <= 2 * R; ++k) {
+        const float wk = a.w[k];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) o[m] = fmaf(wk, v[OFF + k + m], o[m]);
+      }
+      float4* dst = reinterpret_cast<float4*>(h_cur + i * kSTW + 8 * g);
+      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
+    PDZ_P(pf[9] += global_ns() - tph;)
+    PDZ_PT(4, compute_bar());
+    PDZ_P(tph = global_ns();)
 
-      // ---- prefetch Phi / lambda for this thread's outputs into registers
-      float2 phv[8], lmv[8];
-      {
-        const size_t off0 = size_t(cur.yb + j0) * W + gx;
-        const float2* __restrict__ ph =
-            reinterpret_cast<const float2*>(a.phi + cur.p * plane + off0);
-        const float2* __restrict__ lm =
-            reinterpret_cast<const float2*>(a.lam + (cur.p / a.C) * plane + off0);
-        const int rows_here = col_ok ? min(8, cur.n - j0) : 0;
-        const int w2 = W >> 1;  // row stride in float2
+    // ---- vertical pass (FFMA2 over the column pair), divergence, update
+    if (j0 < cur.n) {
+      float2 G2[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) G2[j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 8 + 2 * R; ++k) {
+        const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * kSTW + c);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (j < rows_here) {
-            phv[j] = __ldg(ph + j * w2);
-            lmv[j] = __ldg(lm + j * w2);
-          } else {
-            phv[j] = make_float2(0.f, 0.f);
-            lmv[j] = make_float2(0.f, 0.f);
-          }
+          const int t = k - j;
+          if (t >= 0 && t <= 2 * R) G2[j] = ffma2(make_float2(a.w[t], a.w[t]), hv, G2[j]);
         }
       }
 
-      // ---- wait for this block's input rows; mirror out-of-image columns
-      if (ib) {
-        mbar_wait(bar_cur, phase1);
-        phase1 ^= 1;
-      } else {
-        mbar_wait(bar_cur, phase0);
-        phase0 ^= 1;
-      }
-      const int xbase = cur.x0 - Gm::RP;  // global column of staged column 0
-      if (xbase < 0 || xbase + Gm::PWD > W) {  // border strip (CTA-uniform)
-        const int new0 = cur.first ? 0 : R + 1;
-        const int nnew = cur.first ? cur.n + 2 * R : cur.n;
-        // only the out-of-image staged columns: [0, nl) left, [cr, PWD) right
-        const int nl = xbase < 0 ? -xbase : 0;
-        const int cr = min(Gm::PWD, max(nl, W - xbase));
-        const int nh = nl + (Gm::PWD - cr);
-        for (int k = tid; k < nnew * nh; k += kComputeThreads) {
-          const int i = k / nh, h = k - i * nh;
-          const int ci = h < nl ? h : cr + (h - nl);
-          const int src = reflect(xbase + ci, W) - xbase;
-          if (src >= 0 && src < Gm::PWD)
-            in_cur[(new0 + i) * Gm::PITCH + ci] = in_cur[(new0 + i) * Gm::PITCH + src];
-        }
-        compute_bar();
-      }
-
-      // ---- H rows: carry the 2R overlap, blur the new rows
-      int hnew0, hn, in0row;
-      if (cur.first) {
-        hnew0 = 0;
-        hn = cur.n + 2 * R;
-        in0row = 0;
-      } else {
-        for (int k = tid; k < 2 * R * (kSTW / 4); k += kComputeThreads)
-          reinterpret_cast<float4*>(h_cur)[k] =
-              reinterpret_cast<const float4*>(h_prev + kSRB * kSTW)[k];
-        hnew0 = 2 * R;
-        hn = cur.n;
-        in0row = R + 1;
-      }
-      // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R)
-      // staged values per 8 outputs.
-      for (int item = tid; item < hn * (kSTW / 8); item += kComputeThreads) {
-        const int i = item >> 3, g = item & 7;
-        const float* row = in_cur + (in0row + i) * Gm::PITCH + 8 * g;
-        constexpr int OFF = Gm::RP - R;
-        constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
-        float v[4 * NQ];
+      // rolling window of u rows (A = y-1, B = y, C = y+1) at columns c-1 .. c+2
+      // (staged column RP + c is 8-byte aligned)
+      const float* urow = in_cur + (R + j0 - 1) * Gm::PITCH + Gm::RP + c;
+      const float sx0 = (gx == 0) ? 1.0f : 0.5f;          // column c   (c >= 0)
+      const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;  // column c+1
+      float lA = urow[-1], rA = urow[2];
+      float2 cA = *reinterpret_cast<const float2*>(urow);
+      urow += Gm::PITCH;
+      float lB = urow[-1], rB = urow[2];
+      float2 cB = *reinterpret_cast<const float2*>(urow);
+      float2 xA = make_float2(sx0 * (cA.y - lA), sx1 * (rA - cA.x));
+      float2 xB = make_float2(sx0 * (cB.y - lB), sx1 * (rB - cB.x));
+      // south flux of the row above the first output row
+      float2 fs_up = make_float2(sflux<EDGE>(cB.x - cA.x, 0.5f * (xA.x + xB.x), a.eps),
+                                 sflux<EDGE>(cB.y - cA.y, 0.5f * (xA.y + xB.y), a.eps));
+      float r2 = 0.f;
+      float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + RP;
+      // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
+      // reversed column pair at xm, mirrored row per output row below
+      const int xm = gx < RP ? -2 - gx : (gx >= W - RP ? 2 * W - 2 - gx : kNoMirror);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const float4 t = reinterpret_cast<const float4*>(row)[q];
-          v[4 * q] = t.x;
-          v[4 * q + 1] = t.y;
-          v[4 * q + 2] = t.z;
-          v[4 * q + 3] = t.w;
-        }
-        float o[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) o[m] = 0.f;
-#pragma unroll
-        for (int k = 0; k <= 2 * R; ++k) {
-          const float wk = a.w[k];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) o[m] = fmaf(wk, v[OFF + k + m], o[m]);
-        }
-        float4* dst = reinterpret_cast<float4*>(h_cur + (hnew0 + i) * kSTW + 8 * g);
-        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
-      }
-      compute_bar();
-
-      // ---- queue the next block's rows (+ carry of the R+1 overlap rows)
-      if (have_nxt) {
-        if (!nxt.first) {
-          // rows [nxt.yb - 1, nxt.yb + R) live in in_cur at idx (row - cur_base)
-          const int cur_base = cur.first ? cur.yb - R : cur.yb - 1;
-          const int s0 = (nxt.yb - 1) - cur_base;
-          constexpr int Q = Gm::PWD / 4;
-          for (int k = tid; k < (R + 1) * Q; k += kComputeThreads) {
-            const int i = k / Q, q = k - i * Q;
-            reinterpret_cast<float4*>(in_nxt + i * Gm::PITCH)[q] =
-                reinterpret_cast<const float4*>(in_cur + (s0 + i) * Gm::PITCH)[q];
-          }
-        }
-        if (warp == 0)
-          issue_rows<R>(nxt, uin_all + nxt.p * plane, in_nxt, bar_nxt, H, W, lane);
-      }
-
-      // ---- vertical pass (FFMA2 over the column pair), divergence, update
-      if (j0 < cur.n) {
-        float2 G2[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) G2[j] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < 8 + 2 * R; ++k) {
-          const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * kSTW + c);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int t = k - j;
-            if (t >= 0 && t <= 2 * R) G2[j] = ffma2(make_float2(a.w[t], a.w[t]), hv, G2[j]);
-          }
-        }
-
-        // rolling window of u rows (A = y-1, B = y, C = y+1) at columns c-1 .. c+2
-        // (staged column RP + c is 8-byte aligned)
-        const float* urow = in_cur + ((cur.first ? R : 1) + j0 - 1) * Gm::PITCH + Gm::RP + c;
-        const float sx0 = (gx == 0) ? 1.0f : 0.5f;          // column c   (c >= 0)
-        const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;  // column c+1
-        float lA = urow[-1], rA = urow[2];
-        float2 cA = *reinterpret_cast<const float2*>(urow);
+      for (int j = 0; j < 8; ++j) {
         urow += Gm::PITCH;
-        float lB = urow[-1], rB = urow[2];
-        float2 cB = *reinterpret_cast<const float2*>(urow);
-        float2 xA = make_float2(sx0 * (cA.y - lA), sx1 * (rA - cA.x));
-        float2 xB = make_float2(sx0 * (cB.y - lB), sx1 * (rB - cB.x));
-        // south flux of the row above the first output row
-        float2 fs_up = make_float2(sflux<EDGE>(cB.x - cA.x, 0.5f * (xA.x + xB.x), a.eps),
-                                   sflux<EDGE>(cB.y - cA.y, 0.5f * (xA.y + xB.y), a.eps));
-        float r2 = 0.f;
-        float* __restrict__ uout = uout_all + cur.p * plane;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          urow += Gm::PITCH;
-          const float lC = urow[-1], rC = urow[2];
-          const float2 cC = *reinterpret_cast<const float2*>(urow);
-          const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
-          const int y = cur.yb + j0 + j;
-          const float sy = (y == 0 || y == H - 1) ? 1.0f : 0.5f;
-          // centred vertical differences at columns c-1, c, c+1, c+2
-          const float dl = sy * (lC - lA);
-          const float d0 = sy * (cC.x - cA.x);
-          const float d1 = sy * (cC.y - cA.y);
-          const float dr = sy * (rC - rA);
-          const float u0 = cB.x, u1 = cB.y;
-          const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
-          const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
-          const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
-          const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
-                                           sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
-          const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
-          const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
-          fs_up = fs_dn;
-          lA = lB;
-          rA = rB;
-          cA = cB;
-          xA = xB;
-          lB = lC;
-          rB = rC;
-          cB = cC;
-          xB = xC;
-          const float r0 = fmaf(-lmv[j].x, G2[j].x, div0) + phv[j].x;
-          const float r1 = fmaf(-lmv[j].y, G2[j].y, div1) + phv[j].y;
-          const float n0 = fmaf(a.tau, r0, u0);
-          const float n1 = fmaf(a.tau, r1, u1);
-          if (col_ok && j0 + j < cur.n) {
-            *reinterpret_cast<float2*>(uout + size_t(y) * W + gx) = make_float2(n0, n1);
-            r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
-            acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
+        const float lC = urow[-1], rC = urow[2];
+        const float2 cC = *reinterpret_cast<const float2*>(urow);
+        const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
+        const int y = cur.yb + j0 + j;
+        const float sy = (y == 0 || y == H - 1) ? 1.0f : 0.5f;
+        // centred vertical differences at columns c-1, c, c+1, c+2
+        const float dl = sy * (lC - lA);
+        const float d0 = sy * (cC.x - cA.x);
+        const float d1 = sy * (cC.y - cA.y);
+        const float dr = sy * (rC - rA);
+        const float u0 = cB.x, u1 = cB.y;
+        const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
+        const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
+        const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
+        const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
+                                         sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
+        const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
+        const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
+        fs_up = fs_dn;
+        lA = lB;
+        rA = rB;
+        cA = cB;
+        xA = xB;
+        lB = lC;
+        rB = rC;
+        cB = cC;
+        xB = xC;
+        const float r0 = fmaf(-lmv[j].x, G2[j].x, div0) + phv[j].x;
+        const float r1 = fmaf(-lmv[j].y, G2[j].y, div1) + phv[j].y;
+        const float n0 = fmaf(a.tau, r0, u0);
+        const float n1 = fmaf(a.tau, r1, u1);
+        if (col_ok && j0 + j < cur.n) {
+          *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + gx) = make_float2(n0, n1);
+          const int ym = y < R ? -1 - y : (y >= H - R ? 2 * H - 1 - y : kNoMirror);
+          if (ym != kNoMirror)
+            *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + gx) = make_float2(n0, n1);
+          if (xm != kNoMirror) {
+            *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + xm) = make_float2(n1, n0);
+            if (ym != kNoMirror)
+              *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + xm) = make_float2(n1, n0);
           }
+          r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
+          acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
         }
-        acc_r2 += double(r2);
       }
+      acc_r2 += double(r2);
+    }
 
-      // ---- flush the plane partial when the plane changes / at the end
-      const bool flush = !have_nxt || nxt.p != acc_p;
-      if (flush) {
-        double s = warp_sum(acc_r2);
-        const int nfw = __any_sync(0xffffffffu, !(acc_nf == 0.0f));
-        if (lane == 0) {
-          s_red[warp] = s;
-          s_nf[warp] = nfw;
-        }
-        compute_bar();
-        if (tid == 0) {
-          double t = 0.0;
-          int f = 0;
-#pragma unroll
-          for (int w2 = 0; w2 < kSCW; ++w2) {
-            t += s_red[w2];
-            f |= s_nf[w2];
-          }
-          const int k = int(blockIdx.x - cta_of(int64_t(acc_p) * a.pt.U, S, G));
-          const size_t slot = (size_t(iter % a.pt.ring) * a.P + acc_p) * a.pt.nbmax + k;
-          a.pt.sum[slot] = t;
-          a.pt.flag[slot] = f;
-        }
-        acc_r2 = 0.0;
-        acc_nf = 0.0f;
-        acc_p = have_nxt ? nxt.p : -1;
+    PDZ_P(pf[10] += global_ns() - tph;)
+    // ---- flush the plane partial when the plane changes; publish the pass
+    const bool pass_end = !have_nxt || nxt.pass_start;
+    if (pass_end || nxt.p != cur.p) {
+      double s = warp_sum(acc_r2);
+      const int nfw = __any_sync(0xffffffffu, !(acc_nf == 0.0f));
+      if (lane == 0) {
+        s_red[warp] = s;
+        s_nf[warp] = nfw;
       }
-      cur = nxt;
-      have = have_nxt;
-      ib ^= 1;
+      PDZ_PT(5, compute_bar());  // also orders every output store of the pass before the flag
+      if (tid == 0) {
+        double t = 0.0;
+        int f = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < kSCW; ++w2) {
+          t += s_red[w2];
+          f |= s_nf[w2];
+        }
+        const int k =
+            int(blockIdx.x - cta_of(int64_t(cur.p / a.C) * a.pt.U, S, G));
+        const size_t slot = (size_t(cur.iter % a.pt.ring) * a.P + cur.p) * a.pt.nbmax + k;
+        a.pt.sum[slot] = t;
+        a.pt.flag[slot] = f;
+        if (pass_end) {
+          // passes up to the next pass's predecessor are complete
+          const int done_to = have_nxt ? pass_index(nxt.iter, nxt.c, a.C) - 1 : it.completed(a);
+          st_release_cta_shared(&s_progress, done_to);
+        }
+      }
+      acc_r2 = 0.0;
+      acc_nf = 0.0f;
     }
-    // ---- publish: every output row and partial of this sweep is written
-    // (barrier orders the CTA's writes before thread 0's cumulative fence)
-    compute_bar();
-    if (tid == 0) {
-      __threadfence();
-      st_release(a.done + blockIdx.x, iter);
+    if (nk == kDefer) {
+      PDZ_P(pf[7] += 1;)
+      // the next pass needs this CTA's own progress: published above (the
+      // flush barrier ordered every store of the pass); continue when idle
+      have_nxt = it.next(a, nxt, 0, &s_progress, &s_grant) == kBlock;
+      if (have_nxt && warp == 0) {
+        fence_proxy_async_global();
+        issue_block<R>(a, nxt, ib ? in0 : in1, &bars[ib ^ 1], lane);
+      }
     }
+    cur = nxt;
+    have = have_nxt;
+    ib ^= 1;
+  }
+  if (tid == 0) {
+    st_release_cta_shared(&s_progress, pass_index(a.iter_last, a.C - 1, a.C));
+    st_release_cta_shared(&s_exit, 1);
+    PDZ_P(if (a.prof) {
+      pf[0] = global_ns() - tk0;
+      pf[1] = it.grant_ns;
+      for (int i = 0; i < 16; ++i) a.prof[blockIdx.x * 16 + i] = pf[i];
+    })
   }
 }
 

@@ -25,6 +25,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "pdz_solver.cuh"
 #include "pdz_stream.cuh"
 
@@ -329,14 +331,18 @@ struct Plan {
   int G = 0, nstrips = 0;                   // streaming
   int64_t S = 0, U = 0;
   int nbmax = 0;                            // partial slots per plane
+  int pad_r = 0, pad_c = 0;                 // iterate buffer pads (rows, columns)
   int ring = 2;                             // iteration slots of the partials
   size_t smem = 0;
   void* fn = nullptr;
 };
 
-static int g_force_tiled = -1;  // PDZ_FORCE_TILED=1 -> always the tiled kernel
+static int g_force_tiled = -1;
+#ifdef PDZ_PROFILE
+static long long* g_prof = nullptr;  // tools/prof_stream.py
+#endif  // PDZ_FORCE_TILED=1 -> always the tiled kernel
 
-static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
+static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stream = true) {
   PDZ_REQUIRE(p != nullptr, "params is NULL");
   PDZ_REQUIRE(p->height >= 2 && p->width >= 2, "field must be at least 2x2, got (%d, %d)",
               p->height, p->width);
@@ -361,28 +367,34 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
   const bool edge = p->edge_preserving != 0;
   size_t smem = 0;
   StreamFn sfn = nullptr;
-  const int64_t strip_rows =
-      int64_t((p->width + kSTW - 1) / kSTW) * p->height * int64_t(p->planes);
-  if (!g_force_tiled && p->width % 4 == 0 && strip_rows < (int64_t(1) << 31))
+  const int64_t images = p->planes / p->channels;
+  const int64_t strip_rows = int64_t((p->width + kSTW - 1) / kSTW) * p->height * images;
+  const int rp = (P.R + 3) & ~3;
+  if (allow_stream && !g_force_tiled && p->width % 4 == 0 && p->height >= 2 * P.R &&
+      p->width >= 2 * rp &&
+      strip_rows + p->height < (int64_t(1) << 31))
     sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
   int occ = 0;
   if (sfn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
-  if (sfn && occ >= 1) {
+  if (sfn && int64_t(num_sms()) * occ >= 2) {
     P.stream = true;
+    P.pad_r = P.R;
+    P.pad_c = rp;
     P.fn = reinterpret_cast<void*>(sfn);
     P.smem = smem;
     P.ring = kRing;
     P.nstrips = (p->width + kSTW - 1) / kSTW;
-    P.U = int64_t(P.nstrips) * p->height;
-    P.S = P.U * p->planes;
+    P.U = int64_t(P.nstrips) * p->height;  // strip-rows per image
+    P.S = P.U * images;                    // the C channels share each range
     // Grid size: all CTAs co-resident (cooperative), and CTA ranges aligned to
     // strip boundaries so every CTA pays the same segment-start halo: k CTAs
     // per strip when strips are fewer than slots, else ~equal strips per CTA.
-    const int64_t gmax = int64_t(num_sms()) * occ;
-    const int64_t units = int64_t(P.nstrips) * p->planes;
+    const int64_t gmax = int64_t(num_sms()) * occ - 1;  // + 1 finaliser CTA
+    const int64_t units = int64_t(P.nstrips) * images;
     int64_t G;
     if (units <= gmax) {
-      const int64_t k = std::max<int64_t>(1, std::min<int64_t>(gmax / units, p->height / 16));
+      int64_t k = std::max<int64_t>(1, std::min<int64_t>(gmax / units, p->height / 16));
+      if (const char* e = getenv("PDZ_STREAM_K")) k = std::min<int64_t>(k, atoi(e));  // TEMP
       G = units * k;
     } else {
       const int64_t m = (units + gmax - 1) / gmax;  // strips per CTA
@@ -390,9 +402,9 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl) {
     }
     P.G = int(std::max<int64_t>(1, G));
     int nb = 1;
-    for (int q = 0; q < p->planes; ++q) {
-      const int64_t lo = cta_of(int64_t(q) * P.U, P.S, P.G);
-      const int64_t hi = cta_of(int64_t(q + 1) * P.U - 1, P.S, P.G);
+    for (int64_t q = 0; q < images; ++q) {
+      const int64_t lo = cta_of(q * P.U, P.S, P.G);
+      const int64_t hi = cta_of((q + 1) * P.U - 1, P.S, P.G);
       nb = std::max<int>(nb, int(hi - lo + 1));
     }
     P.nbmax = nb;
@@ -422,6 +434,44 @@ struct Sync {
   int32_t* flags;  // [2]
 };
 
+// TMA tensor maps of the two padded iterate buffers for the streaming kernel:
+// a 3-D tensor [P][H + 2R][W + 2RP] float32, box {64 + 2RP, kSRB + 2R, 1};
+// out-of-bounds elements (over-fetch past the last row) zero-fill.
+static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, float* buf0,
+                                  float* buf1, StreamArgs* b) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PDZ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+             "cuTensorMapEncodeTiled entry point");
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PDZ_ECUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const int R = pl.R;
+  const int pitch = kSTW + 2 * pl.pad_c;
+  const cuuint64_t wp = cuuint64_t(p->width) + 2 * pl.pad_c;
+  const cuuint64_t hp = cuuint64_t(p->height) + 2 * pl.pad_r;
+  const cuuint64_t dims[3] = {wp, hp, cuuint64_t(p->planes)};
+  const cuuint64_t strides[2] = {wp * 4, wp * hp * 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  float* bufs[2] = {buf0, buf1};
+  for (int bi = 0; bi < 2; ++bi) {
+    const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + kSRB), 1};
+    CUresult r = encode(&b->tm[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
+      return PDZ_ECUDA;
+    }
+  }
+  return PDZ_OK;
+}
+
 static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0, float* buf1,
                          const float* phi, const float* lam, double* psum, int32_t* pflag,
                          const StateView& st, const Sync& sy, LaunchArgs* la) {
@@ -445,6 +495,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   pt.S = pl.S;
   pt.U = pl.U;
   pt.G = pl.G;
+  pt.C = pl.stream ? p->channels : 1;
   SweepArgs& a = la->tile;
   a.buf0 = buf0;
   a.buf1 = buf1;
@@ -479,14 +530,24 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.P = p->planes;
   b.C = p->channels;
   b.nstrips = pl.nstrips;
-  b.iter_first = 1;
   b.iter_last = p->max_iters;
   b.max_iters = p->max_iters;
   b.stop_rule = (p->rel_tol >= 0.0) ? 1 : 0;
+#ifdef PDZ_PROFILE
+  if (const char* e = getenv("PDZ_PROF")) {
+    if (e[0] == '1' && pl.stream) {
+      static long long* prof = nullptr;
+      if (!prof) cudaMalloc(&prof, 16 * 8192 * sizeof(long long));
+      b.prof = prof;
+      g_prof = prof;
+    }
+  }
+#endif
   b.eps = float(p->epsilon);
   b.tau = float(p->tau);
   b.rel_tol = p->rel_tol;
   memcpy(b.w, w, sizeof(w));
+  if (pl.stream) return encode_stream_maps(p, pl, buf0, buf1, &b);
   return PDZ_OK;
 }
 
@@ -514,7 +575,7 @@ static int32_t launch_stream(const LaunchArgs& la, const Plan& pl, cudaStream_t 
   cudaLaunchConfig_t cfg = {};
   cfg.stream = s;
   cfg.dynamicSmemBytes = pl.smem;
-  cfg.gridDim = dim3(pl.G);
+  cfg.gridDim = dim3(pl.G + 1);  // + the finaliser CTA
   cfg.blockDim = dim3(kSThreads);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -536,9 +597,41 @@ __global__ void sync_init_kernel(Sync sy, int G) {
   }
 }
 
+// u0 = Phi into a (possibly padded) iterate buffer: pads get the symmetric
+// reflection (solver.py:235) -- one fold, pads <= the image size.
+__global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict__ buf, int H,
+                                int W, int P, int pr, int pc) {
+  const int wp = W + 2 * pc, hp = H + 2 * pr;
+  const int64_t n = int64_t(P) * hp * wp;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pl = i / (int64_t(hp) * wp);
+    const int r = int((i / wp) % hp), q = int(i % wp);
+    const int y = reflect(r - pr, H), x = reflect(q - pc, W);
+    buf[i] = phi[(pl * H + y) * W + x];
+  }
+}
+
+// Dense final iterate: plane p from buf[iters[p] & 1] (the last iteration whose
+// norm was recorded; solver.py:359), interior of the padded layout.
+__global__ void extract_kernel(const float* __restrict__ buf0, const float* __restrict__ buf1,
+                               const int32_t* __restrict__ iters, float* __restrict__ out, int H,
+                               int W, int P, int pr, int pc) {
+  const int wp = W + 2 * pc, hp = H + 2 * pr;
+  const int64_t n = int64_t(P) * H * W;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pl = i / (int64_t(H) * W);
+    const int y = int((i / W) % H), x = int(i % W);
+    const float* src = (iters[pl] & 1) ? buf1 : buf0;
+    out[i] = src[(pl * hp + y + pr) * wp + x + pc];
+  }
+}
+
 struct SolveLayout {
-  float* buf0;
+  float* buf0;  // iterate ping-pong buffers (padded for the streaming kernel)
   float* buf1;
+  float* out;   // dense final iterate [P][H][W] (pdz_fixed_point_sweeps_async)
   double* psum;
   int32_t* pflag;
   StateView st;
@@ -550,9 +643,11 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   Carver c(ws, cap);
   SolveLayout L = {};
   const size_t plane = size_t(p->height) * p->width;
+  const size_t plane_pad = size_t(p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
   const size_t P = p->planes;
-  L.buf0 = c.take<float>(P * plane);
-  L.buf1 = c.take<float>(P * plane);
+  L.buf0 = c.take<float>(P * plane_pad);
+  L.buf1 = c.take<float>(P * plane_pad);
+  L.out = c.take<float>(P * plane);
   L.psum = c.take<double>(size_t(pl.ring) * P * pl.nbmax);
   L.pflag = c.take<int32_t>(size_t(pl.ring) * P * pl.nbmax);
   L.st.stop_iter = c.take<int32_t>(P);
@@ -625,20 +720,37 @@ static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, cons
 // that stops by itself once every plane has stopped.  Tiled: graph chunks;
 // with `poll` the host watches the device `running` counter (lagged by one
 // chunk) and stops queueing once every plane has stopped.
+static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
+                             float* out, cudaStream_t s) {
+  const int64_t n = int64_t(p->planes) * p->height * p->width;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  extract_kernel<<<blocks, 256, 0, s>>>(L.buf0, L.buf1, L.st.iters, out, p->height, p->width,
+                                        p->planes, pl.pad_r, pl.pad_c);
+  PDZ_CHECK_LAUNCH("extract");
+  return PDZ_OK;
+}
+
 static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
-                           const float* phi, const float* lam, cudaStream_t s, bool poll) {
+                           const float* phi, const float* lam, float* out, cudaStream_t s,
+                           bool poll) {
   LaunchArgs la;
   int32_t rc = fill_args(p, pl, L.buf0, L.buf1, phi, lam, L.psum, L.pflag, L.st, L.sy, &la);
   if (rc != PDZ_OK) return rc;
-  const size_t plane_bytes = size_t(p->height) * p->width * sizeof(float);
-  PDZ_CUDA(cudaMemcpyAsync(L.buf0, phi, plane_bytes * p->planes, cudaMemcpyDeviceToDevice, s),
-           "u0 = Phi");
+  {
+    const int64_t n = int64_t(p->planes) * (p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    pad_init_kernel<<<blocks, 256, 0, s>>>(phi, L.buf0, p->height, p->width, p->planes, pl.pad_r,
+                                           pl.pad_c);
+    PDZ_CHECK_LAUNCH("u0 = Phi");
+  }
   init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
   PDZ_CHECK_LAUNCH("init state");
   if (pl.stream) {
     sync_init_kernel<<<(pl.G + 255) / 256, 256, 0, s>>>(L.sy, pl.G);
     PDZ_CHECK_LAUNCH("sync init");
-    return launch_stream(la, pl, s);
+    rc = launch_stream(la, pl, s);
+    if (rc != PDZ_OK) return rc;
+    return queue_extract(p, pl, L, out, s);
   }
 
   cudaGraphExec_t exec;
@@ -682,7 +794,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   PDZ_CUDA(cudaLaunchKernelEx(&cfg, finalize_kernel, L.st, pt, int(p->planes), launched,
                               int(p->max_iters), p->rel_tol),
            "finalize launch");
-  return PDZ_OK;
+  return queue_extract(p, pl, L, out, s);
 }
 
 static int32_t check_abort(const Plan& pl, const Sync& sy) {
@@ -714,16 +826,18 @@ static size_t step_bytes(const pdz_solve_params* params, const Plan& pl) {
 
 size_t pdz_step_workspace_bytes(const pdz_solve_params* params) {
   Plan pl;
-  if (check_params(params, &pl) != PDZ_OK) return 0;
+  if (check_params(params, &pl, false) != PDZ_OK) return 0;
   return step_bytes(params, pl);
 }
 
+// A single sweep over dense caller buffers always runs the tiled kernel (the
+// persistent kernel's padded layout only pays off over many sweeps).
 int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, float* u_out,
                              const float* phi, const float* lambda_map, double* norms,
                              int32_t* nonfinite, void* workspace, size_t workspace_bytes,
                              void* stream) {
   Plan pl;
-  int32_t rc = check_params(params, &pl);
+  int32_t rc = check_params(params, &pl, false);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(u && u_out && phi && lambda_map && norms, "NULL array argument");
   PDZ_REQUIRE(u != u_out, "u_out must not alias u");
@@ -747,13 +861,7 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
                  &la);
   if (rc != PDZ_OK) return rc;
   cudaStream_t s = as_stream(stream);
-  if (pl.stream) {
-    sync_init_kernel<<<1, 256, 0, s>>>(sy, pl.G);
-    PDZ_CHECK_LAUNCH("sync init");
-    rc = launch_stream(la, pl, s);
-  } else {
-    rc = launch_tiled(la, &one, pl, 1, s, false);
-  }
+  rc = launch_tiled(la, &one, pl, 1, s, false);
   if (rc != PDZ_OK) return rc;
   step_norm_kernel<<<1, 256, 0, s>>>(la.tile.pt, params->planes, norms, nonfinite);
   PDZ_CHECK_LAUNCH("step norm");
@@ -783,7 +891,7 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
     return PDZ_EWORKSPACE;
   }
   cudaStream_t s = as_stream(stream);
-  rc = queue_solve(params, pl, L, phi, lambda_map, s, true);
+  rc = queue_solve(params, pl, L, phi, lambda_map, u_out, s, true);
   if (rc != PDZ_OK) return rc;
   const int P = params->planes;
   PDZ_CUDA(cudaStreamSynchronize(s), "solve sync");
@@ -795,17 +903,9 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
   PDZ_CUDA(cudaMemcpy(norms_host, L.st.norms, size_t(params->max_iters) * P * 8,
                       cudaMemcpyDeviceToHost),
            "D2H norms");
-  const size_t plane = size_t(params->height) * params->width;
   int worst = -1;
-  for (int q = 0; q < P; ++q) {
-    const int it = iterations_host[q];
-    const float* src = (it & 1) ? L.buf1 : L.buf0;
-    PDZ_CUDA(cudaMemcpyAsync(u_out + q * plane, src + q * plane, plane * 4,
-                             cudaMemcpyDeviceToDevice, s),
-             "final iterate");
-    if (failed_host[q] != 0 && worst < 0) worst = q;
-  }
-  PDZ_CUDA(cudaStreamSynchronize(s), "solve sync");
+  for (int q = 0; q < P && worst < 0; ++q)
+    if (failed_host[q] != 0) worst = q;
   if (worst >= 0) {
     set_error("solver produced non-finite values at iteration %d (plane %d)", failed_host[worst],
               worst);
@@ -828,7 +928,7 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
     set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
-  return queue_solve(&fixed, pl, L, phi, lambda_map, as_stream(stream), false);
+  return queue_solve(&fixed, pl, L, phi, lambda_map, L.out, as_stream(stream), false);
 }
 
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {
@@ -844,9 +944,20 @@ const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* 
   Plan pl;
   if (check_params(params, &pl) != PDZ_OK || workspace == nullptr) return nullptr;
   SolveLayout L = carve_solve(params, pl, const_cast<void*>(workspace), ~size_t(0) >> 1);
+  (void)iterations;  // the dense copy already holds each plane's final iterate
   const size_t n = size_t(params->height) * params->width;
-  return ((iterations & 1) ? L.buf1 : L.buf0) + plane * n;
+  return L.out + plane * n;
 }
+
+#ifdef PDZ_PROFILE
+// Profiling builds only: per-CTA wait times of the last PDZ_PROF=1 solve.
+int32_t pdz_debug_prof(long long* host, int n) {
+  if (!g_prof) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_prof, size_t(n) * 16 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return 1;
+}
+#endif
 
 int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params) {
   Plan pl;
