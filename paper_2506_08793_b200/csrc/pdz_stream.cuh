@@ -52,27 +52,37 @@
 namespace pdz {
 
 constexpr int kSTW = 64;                    // strip width (output columns)
-constexpr int kSCW = 15;                    // compute warps
-constexpr int kSRB = kSCW * 8;              // output rows per block (8 per warp)
+constexpr int kSCW = 19;                    // compute warps (+1: 640 threads x 96 regs)
+constexpr int kRPW = 6;                     // output rows per compute warp
+constexpr int kSRB = kSCW * kRPW;           // output rows per block
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
 constexpr long long kSpinTimeoutNs = 10000000000ll;
 
+// Shared-memory row pitches are an ODD number of float4s, so the 8 lanes of a
+// quarter-warp that read / write 16 bytes each in 8 different rows of the same
+// column group hit 8 distinct bank quads (conflict-free LDS.128 / STS.128).
 template <int R>
 struct SGeo {
   static constexpr int RP = (R + 3) & ~3;      // column halo rounded to float4
-  static constexpr int PITCH = kSTW + 2 * RP;  // staged floats per row = TMA box width
+  static constexpr int PWD = kSTW + 2 * RP;    // staged floats per row used (even # float4)
+  static constexpr int PITCH = PWD + 4;        // staged row pitch = TMA box width
+  static constexpr int HP = kSTW + 4;          // H row pitch
   static constexpr int ROWS = kSRB + 2 * R;    // staged input rows / H rows = TMA box height
   static constexpr int IN_FLOATS = (ROWS * PITCH + 31) & ~31;  // 128-byte aligned buffers
-  static constexpr int H_FLOATS = (ROWS * kSTW + 31) & ~31;
-  static constexpr size_t SMEM = size_t(2 * IN_FLOATS + H_FLOATS) * 4 + 128;
+  static constexpr int H_FLOATS = (ROWS * HP + 31) & ~31;
+  static constexpr int PL_FLOATS = kSRB * kSTW;  // Phi or lambda tile of the block
+  static constexpr size_t SMEM = size_t(2 * IN_FLOATS + H_FLOATS + 2 * PL_FLOATS) * 4 + 128;
+  static constexpr bool FITS = SMEM <= 227 * 1024;
 };
 
 struct StreamArgs {
   // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2RP], box
   // {PITCH, kSRB + 2R, 1}.
   CUtensorMap tm[2];
+  CUtensorMap tm_phi;   // Phi [P][H][W], box {64, kSRB, 1}
+  CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, kSRB, 1}
   float* buf0;
   float* buf1;
   const float* phi;
@@ -89,6 +99,7 @@ struct StreamArgs {
   double rel_tol;
   long long* prof;      // -DPDZ_PROFILE builds + PDZ_PROF=1: [2G+1][16] wait times
   float w[kMaxTaps];
+  float2 w2[kMaxTaps];  // (w, w) pairs: the FFMA2 operand
 };
 
 // Profiling instrumentation (tools/prof_stream.py): compiled only with
@@ -468,7 +479,7 @@ __device__ void service_loop(const StreamArgs& a, const int* s_progress, const i
       }
       return;
     }
-    __nanosleep(64);
+    __nanosleep(128);  // idle: leave the issue slots to the compute warps
   }
 }
 
@@ -549,14 +560,17 @@ __device__ void finalizer_cta(const StreamArgs& a) {
 
 // ------------------------------------------------------------- kernel --
 template <int R, bool EDGE>
-__global__ void __launch_bounds__(kSThreads, 1)
+__global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     stream_kernel(const __grid_constant__ StreamArgs a) {
   using Gm = SGeo<R>;
   extern __shared__ __align__(128) float smem[];
   float* const in0 = smem;
   float* const in1 = smem + Gm::IN_FLOATS;
   float* const hbuf = smem + 2 * Gm::IN_FLOATS;
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(hbuf + Gm::H_FLOATS);
+  float* const sphi = hbuf + Gm::H_FLOATS;
+  float* const slam = sphi + Gm::PL_FLOATS;
+  // bars[0..1]: IN double buffer; bars[2]: the block's Phi / lambda tiles
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(slam + Gm::PL_FLOATS);
   __shared__ double s_red[kSCW];
   __shared__ int s_nf[kSCW];
   __shared__ int s_progress, s_exit, s_grant;
@@ -565,6 +579,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     mbar_fence_init();
     s_progress = 0;
     s_exit = 0;
@@ -573,7 +588,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
   __syncthreads();
 
   const int H = a.H, W = a.W;
-  const size_t plane = size_t(H) * W;                    // Phi / lambda planes (dense)
   constexpr int RP = Gm::RP;
   const int WP = W + 2 * RP;                             // padded iterate row
   const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
@@ -600,10 +614,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
   PDZ_P(long long tph = 0;)
   PDZ_P(const long long tk0 = global_ns();)
 
-  // thread roles for the vertical pass / update: column pair, 8-row group
-  const int c = 2 * lane;   // strip-local output column of the pair
-  const int j0 = warp * 8;  // block-local first row
-  uint32_t phase0 = 0, phase1 = 0;
+  // thread roles for the vertical pass / update: column pair, kRPW-row group
+  const int c = 2 * lane;      // strip-local output column of the pair
+  const int j0 = warp * kRPW;  // block-local first row
+  uint32_t phase0 = 0, phase1 = 0, phase_pl = 0;
   int ib = 0;
 
   SBlock cur, nxt;
@@ -616,11 +630,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
   float acc_nf = 0.0f;
 
   // Per block b (two CTA barriers):
-  //   barrier (block b-1 finished: IN(b-1) and H are free)
+  //   barrier (block b-1 finished: IN(b-1), H and the Phi / lambda tiles are free)
   //   -> queue IN(b+1) (overlaps all of block b; granted first when b+1
-  //      starts a pass)
+  //      starts a pass) and the Phi / lambda tiles of b (hidden by the H pass)
   //   -> wait IN(b); blur its n + 2R rows into H
-  //   -> barrier
+  //   -> barrier; wait Phi / lambda
   //   -> vertical pass + divergence + update.
   while (have) {
     PDZ_P(const long long tn_ = global_ns();)
@@ -638,33 +652,18 @@ __global__ void __launch_bounds__(kSThreads, 1)
 
     PDZ_PT(2, compute_bar());
     PDZ_P(pf[6] += 1;)
-    if (have_nxt && warp == 0) {
-      if (nxt.pass_start) fence_proxy_async_global();  // granted data -> TMA reads
-      issue_block<R>(a, nxt, in_nxt, bar_nxt, lane);
-    }
-
-    PDZ_P(tph = global_ns();)
-    // ---- prefetch Phi / lambda for this thread's outputs into registers
-    float2 phv[8], lmv[8];
-    {
-      const size_t off0 = size_t(cur.yb + j0) * W + gx;
-      const float2* __restrict__ ph =
-          reinterpret_cast<const float2*>(a.phi + cur.p * plane + off0);
-      const float2* __restrict__ lm =
-          reinterpret_cast<const float2*>(a.lam + (cur.p / a.C) * plane + off0);
-      const int rows_here = col_ok ? min(8, cur.n - j0) : 0;
-      const int w2 = W >> 1;  // row stride in float2
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j < rows_here) {
-          phv[j] = __ldg(ph + j * w2);
-          lmv[j] = __ldg(lm + j * w2);
-        } else {
-          phv[j] = make_float2(0.f, 0.f);
-          lmv[j] = make_float2(0.f, 0.f);
-        }
+    if (warp == 0) {
+      if (have_nxt) {
+        if (nxt.pass_start) fence_proxy_async_global();  // granted data -> TMA reads
+        issue_block<R>(a, nxt, in_nxt, bar_nxt, lane);
+      }
+      if (lane == 0) {  // Phi / lambda tiles of this block (iteration invariant)
+        mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
+        tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
+        tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
       }
     }
+    PDZ_P(tph = global_ns();)
 
     // ---- wait for this block's input rows
     if (ib) {
@@ -678,9 +677,13 @@ __global__ void __launch_bounds__(kSThreads, 1)
     // ---- H rows: horizontal blur of the n + 2R staged rows
     // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R)
     // staged values per 8 outputs.
+    // Item -> (row i, column group g): 8 consecutive items = 8 consecutive rows
+    // of one group (a conflict-free quarter-warp, see SGeo).
     const int hn = cur.n + 2 * R;
-    for (int item = tid; item < hn * (kSTW / 8); item += kComputeThreads) {
-      const int i = item >> 3, g = item & 7;
+    const int hitems = ((hn + 7) & ~7) * (kSTW / 8);
+    for (int item = tid; item < hitems; item += kComputeThreads) {
+      const int i = (item >> 6) * 8 + (item & 7), g = (item >> 3) & 7;
+      if (i >= hn) continue;
       const float* row = in_cur + i * Gm::PITCH + 8 * g;
       constexpr int OFF = Gm::RP - R;
       constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
@@ -693,35 +696,38 @@ __global__ void __launch_bounds__(kSThreads, 1)
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
       }
-      float o[8];
+      // packed FFMA2 over output pairs (per-lane fma.rn, same order as scalar)
+      float2 o[4];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) o[m] = 0.f;
+      for (int m = 0; m < 4; ++m) o[m] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int k = 0; k <= 2 * R; ++k) {
-        const float wk = a.w[k];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) o[m] = fmaf(wk, v[OFF + k + m], o[m]);
+        for (int m = 0; m < 4; ++m)
+          o[m] = ffma2(a.w2[k], make_float2(v[OFF + k + 2 * m], v[OFF + k + 2 * m + 1]), o[m]);
       }
-      float4* dst = reinterpret_cast<float4*>(h_cur + i * kSTW + 8 * g);
-      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+      float4* dst = reinterpret_cast<float4*>(h_cur + i * Gm::HP + 8 * g);
+      dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+      dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
     }
     PDZ_P(pf[9] += global_ns() - tph;)
     PDZ_PT(4, compute_bar());
+    mbar_wait(&bars[2], phase_pl);
+    phase_pl ^= 1;
     PDZ_P(tph = global_ns();)
 
     // ---- vertical pass (FFMA2 over the column pair), divergence, update
     if (j0 < cur.n) {
-      float2 G2[8];
+      float2 G2[kRPW];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) G2[j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < kRPW; ++j) G2[j] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 8 + 2 * R; ++k) {
-        const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * kSTW + c);
+      for (int k = 0; k < kRPW + 2 * R; ++k) {
+        const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * Gm::HP + c);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < kRPW; ++j) {
           const int t = k - j;
-          if (t >= 0 && t <= 2 * R) G2[j] = ffma2(make_float2(a.w[t], a.w[t]), hv, G2[j]);
+          if (t >= 0 && t <= 2 * R) G2[j] = ffma2(a.w2[t], hv, G2[j]);
         }
       }
 
@@ -743,16 +749,24 @@ __global__ void __launch_bounds__(kSThreads, 1)
       float r2 = 0.f;
       float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + RP;
       // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
-      // reversed column pair at xm, mirrored row per output row below
+      // the reversed column pair at xm; rows j < jt also go to row -1-y, rows
+      // j >= jb to row 2H-1-y.  Only threads at an image border take `mir`.
       const int xm = gx < RP ? -2 - gx : (gx >= W - RP ? 2 * W - 2 - gx : kNoMirror);
+      const int y0 = cur.yb + j0;  // image row of j = 0
+      const int jt = R - y0, jb = H - R - y0;
+      const bool mir = jt > 0 || jb < kRPW || xm != kNoMirror;
+      const int jz0 = -y0, jz1 = H - 1 - y0;  // rows 0 / H-1: one-sided differences
+      const int nrows = col_ok ? min(kRPW, cur.n - j0) : 0;
+      float* orow = uout + ptrdiff_t(y0) * WP + gx;
+      const float* pl_row = sphi + j0 * kSTW + c;  // Phi / lambda tiles: row pitch 64
+      const float* lm_row = slam + j0 * kSTW + c;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kRPW; ++j) {
         urow += Gm::PITCH;
         const float lC = urow[-1], rC = urow[2];
         const float2 cC = *reinterpret_cast<const float2*>(urow);
         const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
-        const int y = cur.yb + j0 + j;
-        const float sy = (y == 0 || y == H - 1) ? 1.0f : 0.5f;
+        const float sy = (j == jz0 || j == jz1) ? 1.0f : 0.5f;
         // centred vertical differences at columns c-1, c, c+1, c+2
         const float dl = sy * (lC - lA);
         const float d0 = sy * (cC.x - cA.x);
@@ -775,23 +789,29 @@ __global__ void __launch_bounds__(kSThreads, 1)
         rB = rC;
         cB = cC;
         xB = xC;
-        const float r0 = fmaf(-lmv[j].x, G2[j].x, div0) + phv[j].x;
-        const float r1 = fmaf(-lmv[j].y, G2[j].y, div1) + phv[j].y;
+        const float2 phv = *reinterpret_cast<const float2*>(pl_row + j * kSTW);
+        const float2 lmv = *reinterpret_cast<const float2*>(lm_row + j * kSTW);
+        const float r0 = fmaf(-lmv.x, G2[j].x, div0) + phv.x;
+        const float r1 = fmaf(-lmv.y, G2[j].y, div1) + phv.y;
         const float n0 = fmaf(a.tau, r0, u0);
         const float n1 = fmaf(a.tau, r1, u1);
-        if (col_ok && j0 + j < cur.n) {
-          *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + gx) = make_float2(n0, n1);
-          const int ym = y < R ? -1 - y : (y >= H - R ? 2 * H - 1 - y : kNoMirror);
-          if (ym != kNoMirror)
-            *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + gx) = make_float2(n0, n1);
-          if (xm != kNoMirror) {
-            *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + xm) = make_float2(n1, n0);
+        if (j < nrows) {
+          *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
+          if (mir) {
+            const int y = y0 + j;
+            const int ym = j < jt ? -1 - y : (j >= jb ? 2 * H - 1 - y : kNoMirror);
             if (ym != kNoMirror)
-              *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + xm) = make_float2(n1, n0);
+              *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + gx) = make_float2(n0, n1);
+            if (xm != kNoMirror) {
+              *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + xm) = make_float2(n1, n0);
+              if (ym != kNoMirror)
+                *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + xm) = make_float2(n1, n0);
+            }
           }
           r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
           acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
         }
+        orow += WP;
       }
       acc_r2 += double(r2);
     }
@@ -859,6 +879,7 @@ using StreamFn = void (*)(const StreamArgs);
 
 template <int R, bool EDGE>
 static StreamFn stream_prepared(size_t* smem) {
+  static_assert(SGeo<R>::FITS, "staging buffers exceed shared memory");
   static bool done = false;
   *smem = SGeo<R>::SMEM;
   if (!done) {
@@ -871,14 +892,13 @@ static StreamFn stream_prepared(size_t* smem) {
 
 template <bool EDGE>
 static StreamFn stream_pick(int R, size_t* smem) {
-  switch (R) {
+  switch (R) {  // radii whose staging fits in shared memory (SGeo<R>::FITS)
     case 1: return stream_prepared<1, EDGE>(smem);
     case 2: return stream_prepared<2, EDGE>(smem);
     case 3: return stream_prepared<3, EDGE>(smem);
     case 6: return stream_prepared<6, EDGE>(smem);
     case 9: return stream_prepared<9, EDGE>(smem);
     case 12: return stream_prepared<12, EDGE>(smem);
-    case 24: return stream_prepared<24, EDGE>(smem);
     default: return nullptr;
   }
 }

@@ -20,6 +20,7 @@
 // iteration m is still swept (harmlessly, into the other buffer) at m+1 and
 // skipped from m+2 on, so its answer in buf[m&1] is never overwritten.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -375,7 +376,18 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
       strip_rows + p->height < (int64_t(1) << 31))
     sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
   int occ = 0;
-  if (sfn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
+  if (sfn) {
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
+    if (getenv("PDZ_VERBOSE")) {
+      cudaFuncAttributes fa = {};
+      cudaFuncGetAttributes(&fa, sfn);
+      fprintf(stderr,
+              "pdz: persistent kernel R=%d smem=%zu occupancy=%d (%s) regs=%d maxthreads=%d "
+              "static=%zu maxdyn=%d\n",
+              P.R, smem, occ, cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock,
+              fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+    }
+  }
   if (sfn && int64_t(num_sms()) * occ >= 2) {
     P.stream = true;
     P.pad_r = P.R;
@@ -435,10 +447,11 @@ struct Sync {
 };
 
 // TMA tensor maps of the two padded iterate buffers for the streaming kernel:
-// a 3-D tensor [P][H + 2R][W + 2RP] float32, box {64 + 2RP, kSRB + 2R, 1};
+// a 3-D tensor [P][H + 2R][W + 2RP] float32, box {64 + 2RP + 4, kSRB + 2R, 1};
 // out-of-bounds elements (over-fetch past the last row) zero-fill.
 static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, float* buf0,
-                                  float* buf1, StreamArgs* b) {
+                                  float* buf1, const float* phi, const float* lam,
+                                  StreamArgs* b) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -452,7 +465,7 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, flo
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
   const int R = pl.R;
-  const int pitch = kSTW + 2 * pl.pad_c;
+  const int pitch = kSTW + 2 * pl.pad_c + 4;  // = SGeo<R>::PITCH
   const cuuint64_t wp = cuuint64_t(p->width) + 2 * pl.pad_c;
   const cuuint64_t hp = cuuint64_t(p->height) + 2 * pl.pad_r;
   const cuuint64_t dims[3] = {wp, hp, cuuint64_t(p->planes)};
@@ -466,6 +479,25 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, flo
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
+      return PDZ_ECUDA;
+    }
+  }
+  // Phi [P][H][W] and lambda [P / C][H][W] (dense), box {64, kSRB, 1}
+  const cuuint64_t ddims[2][3] = {
+      {cuuint64_t(p->width), cuuint64_t(p->height), cuuint64_t(p->planes)},
+      {cuuint64_t(p->width), cuuint64_t(p->height), cuuint64_t(p->planes / p->channels)}};
+  const cuuint64_t dstrides[2] = {cuuint64_t(p->width) * 4,
+                                  cuuint64_t(p->width) * p->height * 4};
+  const cuuint32_t dbox[3] = {cuuint32_t(kSTW), cuuint32_t(kSRB), 1};
+  const float* dsrc[2] = {phi, lam};
+  CUtensorMap* dmap[2] = {&b->tm_phi, &b->tm_lam};
+  for (int k = 0; k < 2; ++k) {
+    CUresult r = encode(dmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(dsrc[k]),
+                        ddims[k], dstrides, dbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (Phi / lambda) failed (%d)", int(r));
       return PDZ_ECUDA;
     }
   }
@@ -547,7 +579,8 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.tau = float(p->tau);
   b.rel_tol = p->rel_tol;
   memcpy(b.w, w, sizeof(w));
-  if (pl.stream) return encode_stream_maps(p, pl, buf0, buf1, &b);
+  for (int i = 0; i < kMaxTaps; ++i) b.w2[i] = make_float2(w[i], w[i]);
+  if (pl.stream) return encode_stream_maps(p, pl, buf0, buf1, phi, lam, &b);
   return PDZ_OK;
 }
 
@@ -645,9 +678,9 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   const size_t plane = size_t(p->height) * p->width;
   const size_t plane_pad = size_t(p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
   const size_t P = p->planes;
+  L.out = c.take<float>(P * plane);  // first: same offset under either plan
   L.buf0 = c.take<float>(P * plane_pad);
   L.buf1 = c.take<float>(P * plane_pad);
-  L.out = c.take<float>(P * plane);
   L.psum = c.take<double>(size_t(pl.ring) * P * pl.nbmax);
   L.pflag = c.take<int32_t>(size_t(pl.ring) * P * pl.nbmax);
   L.st.stop_iter = c.take<int32_t>(P);
@@ -868,10 +901,21 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
   return PDZ_OK;
 }
 
+// The plan of a solve: the persistent kernel unless Phi / lambda are not
+// 16-byte aligned (TMA), then the tiled kernel.  The workspace covers both.
+static int32_t solve_plan(const pdz_solve_params* params, const float* phi, const float* lam,
+                          Plan* pl) {
+  const bool aligned =
+      ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(lam)) & 15) == 0;
+  return check_params(params, pl, aligned);
+}
+
 size_t pdz_solve_workspace_bytes(const pdz_solve_params* params) {
-  Plan pl;
+  Plan pl, tl;
   if (check_params(params, &pl) != PDZ_OK) return 0;
-  return Carver::round(carve_solve(params, pl, nullptr, 0).bytes);
+  if (check_params(params, &tl, false) != PDZ_OK) return 0;
+  return Carver::round(std::max(carve_solve(params, pl, nullptr, 0).bytes,
+                                carve_solve(params, tl, nullptr, 0).bytes));
 }
 
 int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
@@ -880,7 +924,7 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
                               int32_t* failed_host, void* workspace, size_t workspace_bytes,
                               void* stream) {
   Plan pl;
-  int32_t rc = check_params(params, &pl);
+  int32_t rc = solve_plan(params, phi, lambda_map, &pl);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(phi && lambda_map && u_out, "NULL array argument");
   PDZ_REQUIRE(norms_host && iterations_host && converged_host && failed_host,
@@ -918,7 +962,7 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
                                      const float* lambda_map, void* workspace,
                                      size_t workspace_bytes, void* stream) {
   Plan pl;
-  int32_t rc = check_params(params, &pl);
+  int32_t rc = solve_plan(params, phi, lambda_map, &pl);
   if (rc != PDZ_OK) return rc;
   PDZ_REQUIRE(phi && lambda_map, "NULL array argument");
   pdz_solve_params fixed = *params;

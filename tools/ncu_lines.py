@@ -5,7 +5,7 @@ import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
-want = sys.argv[2] if len(sys.argv) > 2 else ""
+want = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else ""
 cur_file, hdr = None, None
 inst, stall, text = defaultdict(int), defaultdict(int), {}
 line = None
@@ -31,7 +31,8 @@ for r in rows:
             pass
 ti, ts = sum(inst.values()), sum(stall.values())
 print(f"total inst {ti}  stall samples {ts}")
-for k in sorted(inst, key=lambda k: -stall[k])[:40]:
+key = (lambda k: -inst[k]) if "--by-inst" in sys.argv else (lambda k: -stall[k])
+for k in sorted(inst, key=key)[:40]:
     if want and want not in k[0]:
         continue
     print(f"{k[0].split('/')[-1]:>18}:{k[1]:<4} inst {100*inst[k]/ti:5.1f}%  stall {100*stall[k]/ts:5.1f}%  {text[k].strip()[:80]}")
