@@ -286,43 +286,46 @@ __device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter
 
 enum { kEnd = 0, kBlock = 1, kDefer = 2 };
 constexpr int kNoMirror = -0x40000000;
-constexpr int kGrantAll = 0x7fffffff;
 
-// Compute threads: wait until the service warp has granted pass k (shared
-// memory, CTA scope -- no gpu-scope fence on the compute path).
-__device__ __forceinline__ void wait_grant(const int* s_grant, int k) {
-  while (ld_acquire_cta_shared(s_grant) < k) __nanosleep(20);
+// Spin on a shared-memory value written by the service warp; a wait that
+// outlives the spin timeout traps (the service warp has already flagged the
+// abort) instead of hanging the GPU.
+__device__ __forceinline__ void wait_shared_ge(const int* p, int v) {
+  if (ld_acquire_cta_shared(p) >= v) return;
+  const long long t0 = global_ns();
+  while (ld_acquire_cta_shared(p) < v) {
+    if (global_ns() - t0 > 2 * kSpinTimeoutNs) __trap();
+    __nanosleep(32);
+  }
 }
 
 // Flat stream of (iteration, channel, block).  Passes with no blocks (every
-// plane of the range frozen) are skipped.  `busy` = progress index of the
-// pass of a block still in flight (0: none).  A pass whose grant depends on
-// that pass's completion (its neighbour wait covers this CTA's own pass
-// (n-1, c)) is deferred until the CTA is idle, so a CTA never waits on
-// itself.  When idle, skipped passes are published at once.
+// plane of the range frozen) are skipped.  With the stop rule a pass of
+// iteration n first needs the stop decisions of n - 2 (s_fin, mirrored by the
+// service warp); `busy_iter` = iteration of a block still in flight (0: none)
+// -- a pass whose decisions need that block's own completion is deferred
+// (kDefer) until the CTA is idle, so a CTA never waits on itself.  When idle,
+// skipped passes are published at once.
 struct FlatIter {
   RangeIter r;
   int iter, c;
   bool fresh;  // next block starts a new pass
   bool ended;
   PDZ_P(long long grant_ns;)
-  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy,
-                                      int* s_progress, const int* s_grant) {
+  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy_iter,
+                                      int* s_progress, const int* s_fin) {
     while (!ended && iter <= a.iter_last) {
-      if (fresh) {
-        if (busy && iter >= 2 && pass_index(iter - 1, c, a.C) >= busy) return kDefer;
+      if (fresh && a.stop_rule && a.st.stop_iter && iter > 2) {
+        if (busy_iter && iter - 2 >= busy_iter) return kDefer;
         PDZ_P(const long long tg = global_ns();)
-        wait_grant(s_grant, pass_index(iter, c, a.C));
+        wait_shared_ge(s_fin, iter - 2);
         PDZ_P(grant_ns += global_ns() - tg;)
-        if (a.stop_rule && a.st.stop_iter) {
-          // granted => fin >= iter - 2 (or every plane had stopped); the
-          // all-stopped iteration is published before fin reaches it, so
-          // this test is uniform across threads
-          const int all = ld_relaxed(a.flags);
-          if (all != 0 && all <= iter - 2) {
-            ended = true;
-            break;
-          }
+        // the all-stopped iteration is published before fin reaches it, so
+        // this test is uniform across threads
+        const int all = ld_relaxed(a.flags);
+        if (all != 0 && all <= iter - 2) {
+          ended = true;
+          break;
         }
       }
       if (r.next(a, iter, c, blk)) {
@@ -332,7 +335,8 @@ struct FlatIter {
         fresh = false;
         return kBlock;
       }
-      if (!busy && threadIdx.x == 0) st_release_cta_shared(s_progress, pass_index(iter, c, a.C));
+      if (!busy_iter && threadIdx.x == 0)
+        st_release_cta_shared(s_progress, pass_index(iter, c, a.C));
       if (++c == a.C) {
         c = 0;
         ++iter;
@@ -349,23 +353,27 @@ struct FlatIter {
   }
 };
 
+// A TMA request posted by compute thread 0 for the service warp: load block
+// (p, x0, yb) of iteration `iter`'s input into IN buffer `ib` once pass `k`
+// is granted.
+struct LoadReq {
+  int p, x0, yb, iter, ib, k;
+};
+
 // ----------------------------------------------------------- row loads --
-// Warp 0: queue a block's new input rows with ONE TMA tile load.  The iterate
-// buffers are padded ([P][H + 2R][W + 2RP], the pads holding the symmetric
-// reflection written by the producers), so every needed row and column --
-// image borders included -- is a plain box of the padded tensor.
-// Staged row i holds image row yb - R + i (padded row yb + i); rows beyond the
-// block's n + 2R are over-fetch, never read.
+// ONE TMA tile load brings a block's input rows.  The iterate buffers are
+// padded ([P][H + 2R][W + 2RP], the pads holding the symmetric reflection
+// written by the producers), so every needed row and column -- image borders
+// included -- is a plain box of the padded tensor.  Staged row i holds image
+// row yb - R + i (padded row yb + i); rows beyond the block's n + 2R are
+// over-fetch, never read.
 template <int R>
-__device__ __forceinline__ void issue_block(const StreamArgs& a, const SBlock& b,
-                                            float* in, uint64_t* bar, int lane) {
+__device__ __forceinline__ void issue_block(const StreamArgs& a, const LoadReq& q, float* in,
+                                            uint64_t* bar) {
   using Gm = SGeo<R>;
-  const int buf = (b.iter - 1) & 1;  // the buffer pass `iter` reads
-  if (lane == 0) {
-    mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
-    tma_load_3d(in, &a.tm[buf], b.x0, b.yb, b.p, bar);
-  }
-  __syncwarp();
+  const int buf = (q.iter - 1) & 1;  // the buffer iteration `iter` reads
+  mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
+  tma_load_3d(in, &a.tm[buf], q.x0, q.yb, q.p, bar);
 }
 
 // --------------------------------------------------------- service warp --
@@ -405,40 +413,51 @@ __device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Shared-memory mailbox between the compute warps and the service warp.
+struct Mailbox {
+  int progress;  // passes completed (compute thread 0, after a CTA barrier)
+  int exit;      // compute warps are done
+  int fin;       // mirror of the global `fin` (service warp)
+  int req_seq;   // TMA requests posted (compute thread 0)
+  LoadReq req[2];  // request s in req[s & 1]: at most two outstanding (IN(b), IN(b+1))
+};
+
 // Warp kSCW runs every gpu-scope synchronisation of its CTA, so compute warps
 // never execute a gpu-scope fence (which would wait for their in-flight
-// output stores).  One fence per round serves both directions:
-//  * publish: the compute warps' completed-pass counter (shared memory,
-//    written after a CTA barrier) is released to done[cta];
-//  * grant: pass k = (n, c) may start once the CTAs whose rows it reads have
-//    published pass (n-1, c), partial slot n % kRing is free (fin >= n -
-//    kRing) and, with the stop rule, fin >= n - 2; granted passes are
-//    released to the compute warps through shared memory, up to 3 passes
-//    beyond the published counter.  Once every plane has stopped everything
-//    is granted (the compute warps then end).
-__device__ void service_loop(const StreamArgs& a, const int* s_progress, const int* s_exit,
-                             int* s_grant, const DepSet& dep) {
+// output stores) and never wait for a neighbour -- only for their data.  One
+// fence per round serves every direction:
+//  * publish: the compute warps' completed-pass counter is released to
+//    done[cta];
+//  * load: the posted TMA request for a block of pass k = (n, c) is issued
+//    once k is granted: the CTAs whose rows it reads have published pass
+//    (n-1, c), partial slot n % kRing is free (fin >= n - kRing) and, with the
+//    stop rule, fin >= n - 2 (once every plane has stopped, anything goes);
+//  * fin: with the stop rule, the global `fin` is mirrored for the iterator.
+template <int R>
+__device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float* in1,
+                             uint64_t* bars, const DepSet& dep) {
   const int lane = threadIdx.x & 31;
   const int C = a.C;
   const bool fin_on = a.st.stop_iter != nullptr;
-  const int total = pass_index(a.iter_last, C - 1, C);
-  int published = 0;
-  int granted = 0;
+  const bool mirror_fin = fin_on && a.stop_rule;
+  int published = 0, granted = 0, issued = 0, fin_seen = 0;
   long long t0 = global_ns();
   PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
   PDZ_P(long long t_need = 0;)
   while (true) {
-    const bool last = ld_acquire_cta_shared(s_exit) != 0;  // before the counter:
-    const int x = ld_acquire_cta_shared(s_progress);       // it is final once `last`
+    const bool last = ld_acquire_cta_shared(&mb->exit) != 0;  // before the counter:
+    const int x = ld_acquire_cta_shared(&mb->progress);      // it is final once `last`
+    const int seq = ld_acquire_cta_shared(&mb->req_seq);
     const bool pub = x > published;
-    bool grant = false, all_stopped = false;
-    if (granted < total && granted < x + 3) {
-      const int k = granted + 1;
+    const bool want = seq > issued;
+    const LoadReq q = mb->req[(issued + 1) & 1];  // the next request, in order (valid if `want`)
+    bool grant = false;
+    if (want && q.k > granted) {
       PDZ_P(if (t_need == 0) t_need = global_ns();)
-      const int n = (k - 1) / C + 1;
+      const int n = (q.k - 1) / C + 1;
       bool ok = true;
       if (n >= 2) {
-        const int need = k - C;  // pass (n-1, c)
+        const int need = q.k - C;  // pass (n-1, c)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
           for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
@@ -449,20 +468,32 @@ __device__ void service_loop(const StreamArgs& a, const int* s_progress, const i
         if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
       }
       grant = __all_sync(0xffffffffu, ok);
-      if (!grant && fin_on && a.stop_rule) all_stopped = ld_relaxed(a.flags) != 0;
+      if (!grant && mirror_fin) grant = ld_relaxed(a.flags) != 0;  // every plane stopped
     }
-    if (pub || grant || all_stopped) {
+    int f = 0;
+    if (mirror_fin) f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
+    if (pub || grant || f > fin_seen || (want && q.k <= granted)) {
       PDZ_P(const long long tf_ = global_ns();)
-      fence_acq_rel_gpu();  // release for the publication, acquire for the grant
+      fence_acq_rel_gpu();  // release for the publication, acquire for the rest
       PDZ_P(sp[0] += global_ns() - tf_; sp[1] += 1;)
       if (pub) {
         if (lane == 0) st_relaxed(a.done + blockIdx.x, x);
         published = x;
       }
-      if (grant || all_stopped) {
-        granted = all_stopped ? total : granted + 1;
-        if (lane == 0) st_release_cta_shared(s_grant, all_stopped ? kGrantAll : granted);
+      if (f > fin_seen) {
+        fin_seen = f;
+        if (lane == 0) st_release_cta_shared(&mb->fin, f);
+      }
+      if (grant) {
+        granted = q.k;
         PDZ_P(sp[4] += global_ns() - t_need; sp[5] += 1; t_need = 0;)
+      }
+      if (want && q.k <= granted) {
+        if (lane == 0) {
+          fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
+          issue_block<R>(a, q, q.ib ? in1 : in0, &bars[q.ib]);
+        }
+        issued += 1;
       }
       t0 = global_ns();
       continue;
@@ -473,13 +504,10 @@ __device__ void service_loop(const StreamArgs& a, const int* s_progress, const i
       return;
     }
     if (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs) {
-      if (lane == 0) {
-        atomicExch(a.flags + 1, 1);
-        st_release_cta_shared(s_grant, kGrantAll);
-      }
-      return;
+      if (lane == 0) atomicExch(a.flags + 1, 1);
+      __trap();  // a dependency never arrived: fail the launch rather than hang
     }
-    __nanosleep(128);  // idle: leave the issue slots to the compute warps
+    __nanosleep(want ? 32 : 128);
   }
 }
 
@@ -573,7 +601,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   uint64_t* const bars = reinterpret_cast<uint64_t*>(slam + Gm::PL_FLOATS);
   __shared__ double s_red[kSCW];
   __shared__ int s_nf[kSCW];
-  __shared__ int s_progress, s_exit, s_grant;
+  __shared__ Mailbox mb;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -581,9 +609,10 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
     mbar_fence_init();
-    s_progress = 0;
-    s_exit = 0;
-    s_grant = 0;
+    mb.progress = 0;
+    mb.exit = 0;
+    mb.fin = 0;
+    mb.req_seq = 0;
   }
   __syncthreads();
 
@@ -599,7 +628,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     return;
   }
   if (warp == kSCW) {
-    service_loop(a, &s_progress, &s_exit, &s_grant, dep_set(a, L0, L1, R));
+    service_loop<R>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R));
     return;
   }
 
@@ -620,48 +649,49 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   uint32_t phase0 = 0, phase1 = 0, phase_pl = 0;
   int ib = 0;
 
+  // compute thread 0 posts the TMA request for a block's input rows; the
+  // service warp issues it once the block's pass is granted
+  int req_seq = 0;
+  auto post = [&](const SBlock& b, int buf) {
+    if (tid == 0) {
+      ++req_seq;
+      mb.req[req_seq & 1] = LoadReq{b.p, b.x0, b.yb, b.iter, buf, pass_index(b.iter, b.c, a.C)};
+      st_release_cta_shared(&mb.req_seq, req_seq);
+    }
+  };
+
   SBlock cur, nxt;
-  bool have = it.next(a, cur, 0, &s_progress, &s_grant) == kBlock;
-  if (have && warp == 0) {
-    fence_proxy_async_global();
-    issue_block<R>(a, cur, in0, &bars[0], lane);
-  }
+  bool have = it.next(a, cur, 0, &mb.progress, &mb.fin) == kBlock;
+  if (have) post(cur, 0);
   double acc_r2 = 0.0;
   float acc_nf = 0.0f;
 
   // Per block b (two CTA barriers):
   //   barrier (block b-1 finished: IN(b-1), H and the Phi / lambda tiles are free)
-  //   -> queue IN(b+1) (overlaps all of block b; granted first when b+1
-  //      starts a pass) and the Phi / lambda tiles of b (hidden by the H pass)
+  //   -> post IN(b+1) (the service warp loads it once granted, overlapping
+  //      block b) and queue the Phi / lambda tiles of b (hidden by the H pass)
   //   -> wait IN(b); blur its n + 2R rows into H
   //   -> barrier; wait Phi / lambda
   //   -> vertical pass + divergence + update.
   while (have) {
     PDZ_P(const long long tn_ = global_ns();)
-    const int nk = it.next(a, nxt, pass_index(cur.iter, cur.c, a.C), &s_progress, &s_grant);
+    const int nk = it.next(a, nxt, cur.iter, &mb.progress, &mb.fin);
     PDZ_P(pf[12] += global_ns() - tn_;)
     bool have_nxt = nk == kBlock;
     float* const in_cur = ib ? in1 : in0;
-    float* const in_nxt = ib ? in0 : in1;
     float* const h_cur = hbuf;
     uint64_t* const bar_cur = &bars[ib];
-    uint64_t* const bar_nxt = &bars[ib ^ 1];
     const int gx = cur.x0 + c;
     const bool col_ok = gx < W;
     float* __restrict__ uout_all = (cur.iter & 1) ? a.buf1 : a.buf0;
 
     PDZ_PT(2, compute_bar());
     PDZ_P(pf[6] += 1;)
-    if (warp == 0) {
-      if (have_nxt) {
-        if (nxt.pass_start) fence_proxy_async_global();  // granted data -> TMA reads
-        issue_block<R>(a, nxt, in_nxt, bar_nxt, lane);
-      }
-      if (lane == 0) {  // Phi / lambda tiles of this block (iteration invariant)
-        mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
-        tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
-        tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
-      }
+    if (have_nxt) post(nxt, ib ^ 1);
+    if (tid == 0) {  // Phi / lambda tiles of this block (iteration invariant)
+      mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
+      tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
+      tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
     }
     PDZ_P(tph = global_ns();)
 
@@ -843,7 +873,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         if (pass_end) {
           // passes up to the next pass's predecessor are complete
           const int done_to = have_nxt ? pass_index(nxt.iter, nxt.c, a.C) - 1 : it.completed(a);
-          st_release_cta_shared(&s_progress, done_to);
+          st_release_cta_shared(&mb.progress, done_to);
         }
       }
       acc_r2 = 0.0;
@@ -853,19 +883,16 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       PDZ_P(pf[7] += 1;)
       // the next pass needs this CTA's own progress: published above (the
       // flush barrier ordered every store of the pass); continue when idle
-      have_nxt = it.next(a, nxt, 0, &s_progress, &s_grant) == kBlock;
-      if (have_nxt && warp == 0) {
-        fence_proxy_async_global();
-        issue_block<R>(a, nxt, ib ? in0 : in1, &bars[ib ^ 1], lane);
-      }
+      have_nxt = it.next(a, nxt, 0, &mb.progress, &mb.fin) == kBlock;
+      if (have_nxt) post(nxt, ib ^ 1);
     }
     cur = nxt;
     have = have_nxt;
     ib ^= 1;
   }
   if (tid == 0) {
-    st_release_cta_shared(&s_progress, pass_index(a.iter_last, a.C - 1, a.C));
-    st_release_cta_shared(&s_exit, 1);
+    st_release_cta_shared(&mb.progress, pass_index(a.iter_last, a.C - 1, a.C));
+    st_release_cta_shared(&mb.exit, 1);
     PDZ_P(if (a.prof) {
       pf[0] = global_ns() - tk0;
       pf[1] = it.grant_ns;
