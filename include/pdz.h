@@ -212,13 +212,21 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
 /* Number of kernels pdz_fixed_point_sweeps_async launches for `params`
  * (benchmark bookkeeping). */
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);
-/* Which sweep kernel `params` runs on: 2 = streaming (width % 4 == 0 and a
- * compiled radius), 1 = tiled fallback, -1 = invalid params. */
+/* Which sweep kernel `params` runs on: 2 = persistent (width % 4 == 0,
+ * H >= 2R, W >= 2 ceil4(R), a compiled radius, every CTA co-resident),
+ * 1 = tiled fallback, -1 = invalid params. */
 int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params);
-/* Device pointer to the plane-p final iterate inside a solve workspace after
- * pdz_fixed_point_sweeps_async (buffer parity of `iterations`). */
+/* Device pointer to the plane-p final iterate (dense [H][W]) inside a solve
+ * workspace after pdz_fixed_point_sweeps_async (`iterations` is ignored: the
+ * solve already copied every plane's final iterate into the dense area). */
 const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* workspace,
                                     int32_t plane, int32_t iterations);
+/* Measurement hook: enable != 0 makes later solves record a CUDA event pair
+ * around the sweep kernel launch(es) on the solve's stream;
+ * pdz_last_sweep_kernel_ms() returns the elapsed device time of the last such
+ * solve (synchronising on its end event), or -1 if none was recorded. */
+void pdz_time_sweep_kernels(int32_t enable);
+float pdz_last_sweep_kernel_ms(void);
 
 /* clamp01 + interleave (solver.py:434, image.py:56-61): planar float32 P=C
  * planes -> [H][W][C] float32 or float64 in [0, 1]. */

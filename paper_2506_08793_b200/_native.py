@@ -94,6 +94,8 @@ _SIGNATURES = {
         _i32, [_pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_fixed_point_sweeps_async": (_i32, [_pp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_solve_result_plane": (_vp, [_pp, _vp, _i32, _i32]),
+    "pdz_time_sweep_kernels": (None, [_i32]),
+    "pdz_last_sweep_kernel_ms": (ctypes.c_float, []),
     "pdz_solve_kernel_launches": (_i64, [_pp]),
     "pdz_sweep_kernel_kind": (_i32, [_pp]),
     "pdz_clamp_interleave": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _vp]),

@@ -753,6 +753,21 @@ static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, cons
 // that stops by itself once every plane has stopped.  Tiled: graph chunks;
 // with `poll` the host watches the device `running` counter (lagged by one
 // chunk) and stops queueing once every plane has stopped.
+// Measurement hook (pdz_time_sweep_kernels): events around the sweep launches.
+static bool g_time_kernels = false;
+static cudaEvent_t g_kev[2] = {nullptr, nullptr};
+static bool g_kev_recorded = false;
+
+static void time_mark(int which, cudaStream_t s) {
+  if (!g_time_kernels) return;
+  if (!g_kev[0]) {
+    cudaEventCreate(&g_kev[0]);
+    cudaEventCreate(&g_kev[1]);
+  }
+  cudaEventRecord(g_kev[which], s);
+  if (which == 1) g_kev_recorded = true;
+}
+
 static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
                              float* out, cudaStream_t s) {
   const int64_t n = int64_t(p->planes) * p->height * p->width;
@@ -781,7 +796,9 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   if (pl.stream) {
     sync_init_kernel<<<(pl.G + 255) / 256, 256, 0, s>>>(L.sy, pl.G);
     PDZ_CHECK_LAUNCH("sync init");
+    time_mark(0, s);
     rc = launch_stream(la, pl, s);
+    time_mark(1, s);
     if (rc != PDZ_OK) return rc;
     return queue_extract(p, pl, L, out, s);
   }
@@ -798,6 +815,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
     PDZ_CUDA(cudaEventCreateWithFlags(&events[1], cudaEventDisableTiming), "event");
   }
   int launched = 0;
+  time_mark(0, s);
   for (int c = 0; c < n_chunks; ++c) {
     if (poll && c >= 2) {
       const int slot = (c - 2) & 1;
@@ -814,6 +832,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
       PDZ_CUDA(cudaEventRecord(events[slot], s), "poll record");
     }
   }
+  time_mark(1, s);
   Partials pt = la.tile.pt;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);
@@ -978,9 +997,9 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {
   Plan pl;
   if (check_params(params, &pl) != PDZ_OK) return -1;
-  if (pl.stream) return 3;  // init state + sync init + one persistent launch
+  if (pl.stream) return 5;  // pad init + init state + sync init + persistent + extract
   const int64_t chunks = (params->max_iters + kChunk - 1) / kChunk;
-  return 2 + chunks * (1 + kChunk);  // init + chunk prologues + sweeps + finalize
+  return 4 + chunks * (1 + kChunk);  // pad init + init + chunk prologues + sweeps + finalize + extract
 }
 
 const float* pdz_solve_result_plane(const pdz_solve_params* params, const void* workspace,
@@ -1002,6 +1021,16 @@ int32_t pdz_debug_prof(long long* host, int n) {
   return 1;
 }
 #endif
+
+void pdz_time_sweep_kernels(int32_t enable) { g_time_kernels = enable != 0; }
+
+float pdz_last_sweep_kernel_ms(void) {
+  if (!g_kev_recorded) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(g_kev[1]) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, g_kev[0], g_kev[1]) != cudaSuccess) return -1.0f;
+  return ms;
+}
 
 int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params) {
   Plan pl;
