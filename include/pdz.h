@@ -177,6 +177,20 @@ int32_t pdz_gaussian_f64(const pdz_solve_params* params, const double* u, double
 /* ---- relaxed fixed-point sweep (the hot kernel) ------------------------- */
 size_t pdz_step_workspace_bytes(const pdz_solve_params* params);
 
+/* One sweep of a ROW SLAB of a larger image (multi-GPU row-slab mode, SURVEY
+ * 8(e); paper_2506_08793_b200/parallel.py).  `params->height` rows of u /
+ * Phi / lambda are given; array row y is global row y + row_offset of a
+ * global_height-row image.  The caller fills the halo rows (neighbour rows,
+ * or the symmetric reflection at the global top / bottom); only rows
+ * [row_lo, row_hi) are written to u_out and counted.  Per plane,
+ * sumsq[p] = sum of r^2 over those rows (the caller all-reduces and takes the
+ * square root, solver.py:301), nonfinite[p] as in pdz_fixed_point_step.
+ * Workspace: pdz_step_workspace_bytes(params). */
+int32_t pdz_fixed_point_step_rows(const pdz_solve_params* params, const float* u, float* u_out,
+                                  const float* phi, const float* lambda_map, int32_t row_offset,
+                                  int32_t global_height, int32_t row_lo, int32_t row_hi,
+                                  double* sumsq, int32_t* nonfinite, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 /* fixed_point_step (solver.py:280-302) on all P planes at once: one fused
  * sweep u_out = u + tau * r, r = div(D grad u) - lambda G(u) + Phi, with
  * ||r||_2 per plane (device float64[P]) and a per-plane non-finite flag

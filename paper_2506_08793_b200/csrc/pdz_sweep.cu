@@ -49,6 +49,10 @@ struct SweepArgs {
   int32_t tiles_x, nblk;
   int32_t iter_off;      // iteration = (*st.iter_base if set) + iter_off
   int32_t max_iters;
+  // Row slab of a larger image (pdz_fixed_point_step_rows): array row y is
+  // global row y + y_off of an H_glob-row image; only rows [row_lo, row_hi)
+  // are written and counted in the norms.  Whole image: 0, H, 0, H.
+  int32_t y_off, H_glob, row_lo, row_hi;
   float eps, tau;
   double rel_tol;
   float w[kMaxTaps];     // 1-D Gaussian taps (kernel params -> constant bank)
@@ -198,7 +202,8 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
 #pragma unroll
   for (int j = 0; j < kRowsPerWarp; ++j) {
     const int gy = y0 + j0 + j;
-    const float sy = (gy == 0 || gy == H - 1) ? 1.0f : 0.5f;
+    const int yg = gy + a.y_off;  // global row (np.gradient ends: solver.py:178-179)
+    const float sy = (yg == 0 || yg == a.H_glob - 1) ? 1.0f : 0.5f;
     const float cy0 = sy * (U[j + 2][0] - U[j][0]);
     const float cy1 = sy * (U[j + 2][1] - U[j][1]);
     const float cy2 = sy * (U[j + 2][2] - U[j][2]);
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
         face_flux<EDGE>(U[j + 2][1] - U[j + 1][1], 0.5f * (cx[j + 1] + cx[j + 2]), a.eps);
     const float div = ((fe_r - fe_l) + fs_dn) - fs_up;
     fs_up = fs_dn;
-    if (gy < H && gx < W) {
+    if (gy >= a.row_lo && gy < a.row_hi && gx < W) {
       const size_t off = size_t(gy) * W + gx;
       const float r = fmaf(-lam[off], G[j], div) + phi[off];
       const float un = fmaf(a.tau, r, U[j + 1][1]);
@@ -273,7 +278,8 @@ __global__ void init_state_kernel(StateView st, int P) {
 }
 
 // Single fixed_point_step: norms[p] = sqrt(sum of the iteration-1 partials).
-__global__ void step_norm_kernel(Partials pt, int P, double* norms, int32_t* nonfinite) {
+__global__ void step_norm_kernel(Partials pt, int P, double* norms, int32_t* nonfinite,
+                                 int take_sqrt) {
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
     const size_t base = (size_t(1 % pt.ring) * P + p) * pt.nbmax;
     const int n = partial_count(pt, p);
@@ -283,7 +289,7 @@ __global__ void step_norm_kernel(Partials pt, int P, double* norms, int32_t* non
       s += pt.sum[base + b];
       nf |= pt.flag[base + b];
     }
-    norms[p] = sqrt(s);
+    norms[p] = take_sqrt ? sqrt(s) : s;
     if (nonfinite) nonfinite[p] = nf;
   }
 }
@@ -546,6 +552,10 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   a.eps = float(p->epsilon);
   a.tau = float(p->tau);
   a.rel_tol = p->rel_tol;
+  a.y_off = 0;
+  a.H_glob = p->height;
+  a.row_lo = 0;
+  a.row_hi = p->height;
   memcpy(a.w, w, sizeof(w));
   StreamArgs& b = la->stream;
   b.buf0 = buf0;
@@ -882,16 +892,18 @@ size_t pdz_step_workspace_bytes(const pdz_solve_params* params) {
   return step_bytes(params, pl);
 }
 
-// A single sweep over dense caller buffers always runs the tiled kernel (the
-// persistent kernel's padded layout only pays off over many sweeps).
-int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, float* u_out,
-                             const float* phi, const float* lambda_map, double* norms,
-                             int32_t* nonfinite, void* workspace, size_t workspace_bytes,
-                             void* stream) {
+// One tiled sweep over dense caller buffers (shared by the whole-image step
+// and the row-slab step).  `out` receives sqrt(sum r^2) (take_sqrt) or the raw
+// sum of r^2 over rows [row_lo, row_hi) per plane.
+static int32_t step_impl(const pdz_solve_params* params, const float* u, float* u_out,
+                         const float* phi, const float* lambda_map, int32_t y_off,
+                         int32_t H_glob, int32_t row_lo, int32_t row_hi, double* out,
+                         int32_t* nonfinite, int take_sqrt, void* workspace,
+                         size_t workspace_bytes, void* stream) {
   Plan pl;
   int32_t rc = check_params(params, &pl, false);
   if (rc != PDZ_OK) return rc;
-  PDZ_REQUIRE(u && u_out && phi && lambda_map && norms, "NULL array argument");
+  PDZ_REQUIRE(u && u_out && phi && lambda_map && out, "NULL array argument");
   PDZ_REQUIRE(u != u_out, "u_out must not alias u");
   Carver c(workspace, workspace_bytes);
   double* psum = c.take<double>(size_t(pl.ring) * params->planes * pl.nbmax);
@@ -912,12 +924,44 @@ int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, flo
   rc = fill_args(&one, pl, const_cast<float*>(u), u_out, phi, lambda_map, psum, pflag, none, sy,
                  &la);
   if (rc != PDZ_OK) return rc;
+  la.tile.y_off = y_off;
+  la.tile.H_glob = H_glob;
+  la.tile.row_lo = row_lo;
+  la.tile.row_hi = row_hi;
   cudaStream_t s = as_stream(stream);
   rc = launch_tiled(la, &one, pl, 1, s, false);
   if (rc != PDZ_OK) return rc;
-  step_norm_kernel<<<1, 256, 0, s>>>(la.tile.pt, params->planes, norms, nonfinite);
+  step_norm_kernel<<<1, 256, 0, s>>>(la.tile.pt, params->planes, out, nonfinite, take_sqrt);
   PDZ_CHECK_LAUNCH("step norm");
   return PDZ_OK;
+}
+
+// A single sweep over dense caller buffers always runs the tiled kernel (the
+// persistent kernel's padded layout only pays off over many sweeps).
+int32_t pdz_fixed_point_step(const pdz_solve_params* params, const float* u, float* u_out,
+                             const float* phi, const float* lambda_map, double* norms,
+                             int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  PDZ_REQUIRE(params != nullptr, "params is NULL");
+  return step_impl(params, u, u_out, phi, lambda_map, 0, params->height, 0, params->height,
+                   norms, nonfinite, 1, workspace, workspace_bytes, stream);
+}
+
+int32_t pdz_fixed_point_step_rows(const pdz_solve_params* params, const float* u, float* u_out,
+                                  const float* phi, const float* lambda_map, int32_t row_offset,
+                                  int32_t global_height, int32_t row_lo, int32_t row_hi,
+                                  double* sumsq, int32_t* nonfinite, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  PDZ_REQUIRE(params != nullptr, "params is NULL");
+  PDZ_REQUIRE(global_height >= 2, "global_height must be >= 2, got %d", global_height);
+  PDZ_REQUIRE(row_lo >= 1 && row_hi <= params->height - 1 && row_lo < row_hi,
+              "row window [%d, %d) must leave >= 1 halo row on both sides of %d rows", row_lo,
+              row_hi, params->height);
+  PDZ_REQUIRE(row_offset + row_lo >= 0 && row_offset + row_hi <= global_height,
+              "rows [%d, %d) + offset %d fall outside the %d-row image", row_lo, row_hi,
+              row_offset, global_height);
+  return step_impl(params, u, u_out, phi, lambda_map, row_offset, global_height, row_lo, row_hi,
+                   sumsq, nonfinite, 0, workspace, workspace_bytes, stream);
 }
 
 // The plan of a solve: the persistent kernel unless Phi / lambda are not
