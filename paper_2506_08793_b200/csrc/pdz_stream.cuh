@@ -46,6 +46,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "pdz_solver.cuh"
 
@@ -358,6 +359,7 @@ struct FlatIter {
 // is granted.
 struct LoadReq {
   int p, x0, yb, iter, ib, k;
+  PDZ_P(long long t_post;)
 };
 
 // ----------------------------------------------------------- row loads --
@@ -463,11 +465,13 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
           for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
             ok &= ld_relaxed(a.done + j) >= need;
       }
+      PDZ_P(const bool ok_dep = __all_sync(0xffffffffu, ok);)
       if (lane == 0 && fin_on) {
         const int need_fin = a.stop_rule ? n - 2 : n - kRing;
         if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
       }
       grant = __all_sync(0xffffffffu, ok);
+      PDZ_P(if (!ok_dep) sp[6] += 1; else if (!grant) sp[7] += 1;)
       if (!grant && mirror_fin) grant = ld_relaxed(a.flags) != 0;  // every plane stopped
     }
     int f = 0;
@@ -492,6 +496,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         if (lane == 0) {
           fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
           issue_block<R>(a, q, q.ib ? in1 : in0, &bars[q.ib]);
+          PDZ_P(sp[2] += global_ns() - q.t_post; sp[3] += 1;)
         }
         issued += 1;
       }
@@ -655,7 +660,8 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   auto post = [&](const SBlock& b, int buf) {
     if (tid == 0) {
       ++req_seq;
-      mb.req[req_seq & 1] = LoadReq{b.p, b.x0, b.yb, b.iter, buf, pass_index(b.iter, b.c, a.C)};
+      mb.req[req_seq & 1] = LoadReq{b.p, b.x0, b.yb, b.iter, buf, pass_index(b.iter, b.c, a.C)
+                                    PDZ_P(, global_ns())};
       st_release_cta_shared(&mb.req_seq, req_seq);
     }
   };
@@ -779,8 +785,9 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       float r2 = 0.f;
       float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + RP;
       // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
-      // the reversed column pair at xm; rows j < jt also go to row -1-y, rows
-      // j >= jb to row 2H-1-y.  Only threads at an image border take `mir`.
+      // the reversed column pair at column xm; rows j < jt also go to row
+      // -1-y, rows j >= jb to row 2H-1-y.  Warps without a border thread run
+      // the loop without any mirror code (warp-uniform choice).
       const int xm = gx < RP ? -2 - gx : (gx >= W - RP ? 2 * W - 2 - gx : kNoMirror);
       const int y0 = cur.yb + j0;  // image row of j = 0
       const int jt = R - y0, jb = H - R - y0;
@@ -790,59 +797,69 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       float* orow = uout + ptrdiff_t(y0) * WP + gx;
       const float* pl_row = sphi + j0 * kSTW + c;  // Phi / lambda tiles: row pitch 64
       const float* lm_row = slam + j0 * kSTW + c;
+      auto rows = [&](auto mirror_tag) {
+        constexpr bool MIR = decltype(mirror_tag)::value;
+        const int dx = xm != kNoMirror ? xm - gx : 0;  // column offset of the mirror pair
+        float* const top = uout + ptrdiff_t(-1 - y0) * WP + gx;  // row -1-y at j = 0
+        float* const bot = uout + ptrdiff_t(2 * H - 1 - y0) * WP + gx;  // row 2H-1-y
 #pragma unroll
-      for (int j = 0; j < kRPW; ++j) {
-        urow += Gm::PITCH;
-        const float lC = urow[-1], rC = urow[2];
-        const float2 cC = *reinterpret_cast<const float2*>(urow);
-        const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
-        const float sy = (j == jz0 || j == jz1) ? 1.0f : 0.5f;
-        // centred vertical differences at columns c-1, c, c+1, c+2
-        const float dl = sy * (lC - lA);
-        const float d0 = sy * (cC.x - cA.x);
-        const float d1 = sy * (cC.y - cA.y);
-        const float dr = sy * (rC - rA);
-        const float u0 = cB.x, u1 = cB.y;
-        const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
-        const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
-        const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
-        const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
-                                         sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
-        const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
-        const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
-        fs_up = fs_dn;
-        lA = lB;
-        rA = rB;
-        cA = cB;
-        xA = xB;
-        lB = lC;
-        rB = rC;
-        cB = cC;
-        xB = xC;
-        const float2 phv = *reinterpret_cast<const float2*>(pl_row + j * kSTW);
-        const float2 lmv = *reinterpret_cast<const float2*>(lm_row + j * kSTW);
-        const float r0 = fmaf(-lmv.x, G2[j].x, div0) + phv.x;
-        const float r1 = fmaf(-lmv.y, G2[j].y, div1) + phv.y;
-        const float n0 = fmaf(a.tau, r0, u0);
-        const float n1 = fmaf(a.tau, r1, u1);
-        if (j < nrows) {
-          *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
-          if (mir) {
-            const int y = y0 + j;
-            const int ym = j < jt ? -1 - y : (j >= jb ? 2 * H - 1 - y : kNoMirror);
-            if (ym != kNoMirror)
-              *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + gx) = make_float2(n0, n1);
-            if (xm != kNoMirror) {
-              *reinterpret_cast<float2*>(uout + ptrdiff_t(y) * WP + xm) = make_float2(n1, n0);
-              if (ym != kNoMirror)
-                *reinterpret_cast<float2*>(uout + ptrdiff_t(ym) * WP + xm) = make_float2(n1, n0);
+        for (int j = 0; j < kRPW; ++j) {
+          urow += Gm::PITCH;
+          const float lC = urow[-1], rC = urow[2];
+          const float2 cC = *reinterpret_cast<const float2*>(urow);
+          const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
+          const float sy = (j == jz0 || j == jz1) ? 1.0f : 0.5f;
+          // centred vertical differences at columns c-1, c, c+1, c+2
+          const float dl = sy * (lC - lA);
+          const float d0 = sy * (cC.x - cA.x);
+          const float d1 = sy * (cC.y - cA.y);
+          const float dr = sy * (rC - rA);
+          const float u0 = cB.x, u1 = cB.y;
+          const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
+          const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
+          const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
+          const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
+                                           sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
+          const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
+          const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
+          fs_up = fs_dn;
+          lA = lB;
+          rA = rB;
+          cA = cB;
+          xA = xB;
+          lB = lC;
+          rB = rC;
+          cB = cC;
+          xB = xC;
+          const float2 phv = *reinterpret_cast<const float2*>(pl_row + j * kSTW);
+          const float2 lmv = *reinterpret_cast<const float2*>(lm_row + j * kSTW);
+          const float r0 = fmaf(-lmv.x, G2[j].x, div0) + phv.x;
+          const float r1 = fmaf(-lmv.y, G2[j].y, div1) + phv.y;
+          const float n0 = fmaf(a.tau, r0, u0);
+          const float n1 = fmaf(a.tau, r1, u1);
+          if (j < nrows) {
+            *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
+            if (MIR) {
+#ifndef PDZ_NO_MIRROR_STORES  // (profiling experiment only)
+              const bool ym = j < jt || j >= jb;
+              float* const mrow = (j < jt ? top : bot) - ptrdiff_t(j) * WP;
+              if (ym) *reinterpret_cast<float2*>(mrow) = make_float2(n0, n1);
+              if (dx != 0) {
+                *reinterpret_cast<float2*>(orow + dx) = make_float2(n1, n0);
+                if (ym) *reinterpret_cast<float2*>(mrow + dx) = make_float2(n1, n0);
+              }
+#endif
             }
+            r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
+            acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
           }
-          r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
-          acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
+          orow += WP;
         }
-        orow += WP;
-      }
+      };
+      if (__any_sync(0xffffffffu, mir))
+        rows(std::true_type{});
+      else
+        rows(std::false_type{});
       acc_r2 += double(r2);
     }
 

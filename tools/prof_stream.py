@@ -38,7 +38,7 @@ torch.cuda.synchronize()
 buf = np.zeros((8192, 16), dtype=np.int64)
 lib.pdz_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lib.pdz_debug_prof(buf.ctypes.data, 8192)
-G = int((buf[:4096, 6] > 0).sum())
+G = int(((buf[:4096, 6] > 0) & (buf[:4096, 12] > 0)).sum())
 g = buf[:G]
 sv = buf[G + 1:2 * G + 1]
 names = ["total", "grant", "topbar", "mbar", "hbar", "flushbar", "blocks", "defers",
@@ -47,15 +47,16 @@ print(f"G={len(g)}  iters={iters}  per-sweep us (mean / min / max over CTAs):")
 for i, n in enumerate(names):
     v = g[:, i] / iters if i in (6, 7) else g[:, i] / (1e3 * iters)
     print(f"  {n:9s} {v.mean():8.3f} {v.min():8.3f} {v.max():8.3f}")
-snames = ["fence_ns", "fences", "final_ns", "finals", "grantlat", "grants"]
+snames = ["fence_ns", "fences", "post2issue", "issues", "grantlat", "grants", "depfail", "finfail"]
 print("service warp per sweep (mean / min / max):")
 for i, n in enumerate(snames):
     v = sv[:, i] / iters
     if i in (0, 2, 4):
         v = v / 1e3
+    if i == 2:
+        v = sv[:, 2] / np.maximum(sv[:, 3], 1) / 1e3  # per issue
     print(f"  {n:9s} {v.mean():8.3f} {v.min():8.3f} {v.max():8.3f}")
-print("  fence us each", (sv[:, 0].sum() / max(1, sv[:, 1].sum())) / 1e3,
-      " finalize us each", (sv[:, 2].sum() / max(1, sv[:, 3].sum())) / 1e3)
+print("  fence us each", (sv[:, 0].sum() / max(1, sv[:, 1].sum())) / 1e3)
 S = ((size + 63) // 64) * size
 order = np.argsort(g[:, 1])
 print("slowest CTAs (least grant wait): cta strip y0 y1 grant_us/sweep")
@@ -70,3 +71,10 @@ for i in order[-5:]:
     print(f"  {i:4d} strip {L0 // size:2d} rows {L0 % size:4d}-{(L1 - 1) % size:4d}  " +
           " ".join(f"{n}={g[i, j] / 1e3 / iters:6.2f}" for j, n in enumerate(names)
                    if j not in (0, 6, 7)))
+print("slowest CTAs by vpass:")
+for i in np.argsort(-g[:, 10])[:16]:
+    L0, L1 = i * S // G, (i + 1) * S // G
+    print(f"  {i:4d} strip {L0 // size:2d} rows {L0 % size:4d}-{(L1 - 1) % size:4d}  "
+          f"vpass={g[i, 10] / 1e3 / iters:6.2f} hpass={g[i, 9] / 1e3 / iters:6.2f} "
+          f"mbar={g[i, 3] / 1e3 / iters:6.2f}")
+print("fastest by vpass:", ", ".join(f"{i}:{g[i, 10] / 1e3 / iters:.2f}" for i in np.argsort(g[:, 10])[:6]))
