@@ -59,6 +59,10 @@ constexpr int kSRB = kSCW * kRPW;           // output rows per block
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
+// Column pad of the padded iterates: 32 floats (128 B) each side, so padded
+// rows and every strip's first image column are 128-byte aligned (only the
+// ceil4(R) columns next to the image are ever written or read).
+constexpr int kPadC = 32;
 constexpr long long kSpinTimeoutNs = 10000000000ll;
 
 // Shared-memory row pitches are an ODD number of float4s, so the 8 lanes of a
@@ -79,7 +83,7 @@ struct SGeo {
 };
 
 struct StreamArgs {
-  // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2RP], box
+  // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2 kPadC], box
   // {PITCH, kSRB + 2R, 1}.
   CUtensorMap tm[2];
   CUtensorMap tm_phi;   // Phi [P][H][W], box {64, kSRB, 1}
@@ -364,7 +368,7 @@ struct LoadReq {
 
 // ----------------------------------------------------------- row loads --
 // ONE TMA tile load brings a block's input rows.  The iterate buffers are
-// padded ([P][H + 2R][W + 2RP], the pads holding the symmetric reflection
+// padded ([P][H + 2R][W + 2 kPadC], the pads holding the symmetric reflection
 // written by the producers), so every needed row and column -- image borders
 // included -- is a plain box of the padded tensor.  Staged row i holds image
 // row yb - R + i (padded row yb + i); rows beyond the block's n + 2R are
@@ -375,7 +379,7 @@ __device__ __forceinline__ void issue_block(const StreamArgs& a, const LoadReq& 
   using Gm = SGeo<R>;
   const int buf = (q.iter - 1) & 1;  // the buffer iteration `iter` reads
   mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
-  tma_load_3d(in, &a.tm[buf], q.x0, q.yb, q.p, bar);
+  tma_load_3d(in, &a.tm[buf], q.x0 + kPadC - Gm::RP, q.yb, q.p, bar);
 }
 
 // --------------------------------------------------------- service warp --
@@ -623,7 +627,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
 
   const int H = a.H, W = a.W;
   constexpr int RP = Gm::RP;
-  const int WP = W + 2 * RP;                             // padded iterate row
+  const int WP = W + 2 * kPadC;                          // padded iterate row
   const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
   const int S = int(a.pt.S), G = a.pt.G;
   const int L0 = int(cta_start(blockIdx.x, S, G));
@@ -783,7 +787,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       float2 fs_up = make_float2(sflux<EDGE>(cB.x - cA.x, 0.5f * (xA.x + xB.x), a.eps),
                                  sflux<EDGE>(cB.y - cA.y, 0.5f * (xA.y + xB.y), a.eps));
       float r2 = 0.f;
-      float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + RP;
+      float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + kPadC;
       // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
       // the reversed column pair at column xm; rows j < jt also go to row
       // -1-y, rows j >= jb to row 2H-1-y.  Warps without a border thread run

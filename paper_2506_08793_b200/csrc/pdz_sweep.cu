@@ -397,7 +397,7 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
   if (sfn && int64_t(num_sms()) * occ >= 2) {
     P.stream = true;
     P.pad_r = P.R;
-    P.pad_c = rp;
+    P.pad_c = kPadC;
     P.fn = reinterpret_cast<void*>(sfn);
     P.smem = smem;
     P.ring = kRing;
@@ -453,7 +453,7 @@ struct Sync {
 };
 
 // TMA tensor maps of the two padded iterate buffers for the streaming kernel:
-// a 3-D tensor [P][H + 2R][W + 2RP] float32, box {64 + 2RP + 4, kSRB + 2R, 1};
+// a 3-D tensor [P][H + 2R][W + 2 kPadC] float32, box {64 + 2RP + 4, kSRB + 2R, 1};
 // out-of-bounds elements (over-fetch past the last row) zero-fill.
 static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, float* buf0,
                                   float* buf1, const float* phi, const float* lam,
@@ -471,7 +471,7 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, flo
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
   const int R = pl.R;
-  const int pitch = kSTW + 2 * pl.pad_c + 4;  // = SGeo<R>::PITCH
+  const int pitch = kSTW + 2 * ((R + 3) & ~3) + 4;  // = SGeo<R>::PITCH
   const cuuint64_t wp = cuuint64_t(p->width) + 2 * pl.pad_c;
   const cuuint64_t hp = cuuint64_t(p->height) + 2 * pl.pad_r;
   const cuuint64_t dims[3] = {wp, hp, cuuint64_t(p->planes)};

@@ -47,11 +47,11 @@ print(f"G={len(g)}  iters={iters}  per-sweep us (mean / min / max over CTAs):")
 for i, n in enumerate(names):
     v = g[:, i] / iters if i in (6, 7) else g[:, i] / (1e3 * iters)
     print(f"  {n:9s} {v.mean():8.3f} {v.min():8.3f} {v.max():8.3f}")
-snames = ["fence_ns", "fences", "post2issue", "issues", "grantlat", "grants", "depfail", "finfail"]
+snames = ["fence_ns", "fences", "post2issue", "issues", "grantlat", "waitwr_ns", "depfail", "store_ns"]
 print("service warp per sweep (mean / min / max):")
 for i, n in enumerate(snames):
     v = sv[:, i] / iters
-    if i in (0, 2, 4):
+    if i in (0, 2, 4, 5, 7):
         v = v / 1e3
     if i == 2:
         v = sv[:, 2] / np.maximum(sv[:, 3], 1) / 1e3  # per issue
