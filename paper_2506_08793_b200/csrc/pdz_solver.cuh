@@ -36,6 +36,11 @@ struct Partials {
   int64_t U;      // v2: strip-rows per image (strips x H)
   int32_t G;      // v2: grid size
   int32_t C;      // v2: planes per image (the C channels share the CTA ranges)
+  // per-strip partition (kps > 0): strip s of an image gets kps CTAs, plus
+  // `bonus` for the two border strips (their mirrored pad stores make a row
+  // dearer); within a strip the rows are split evenly.  kps == 0: the S
+  // strip-rows are split into G even ranges (several strips per CTA).
+  int32_t kps, bonus, nstr, H;
 };
 
 // Index of the CTA whose balanced range [floor(iS/G), floor((i+1)S/G)) holds
@@ -47,11 +52,45 @@ __host__ __device__ __forceinline__ int64_t cta_start(int64_t i, int64_t S, int6
   return (i * S) / G;
 }
 
+// CTAs of one image in the per-strip partition.
+__host__ __device__ __forceinline__ int64_t part_per_image(const Partials& pt) {
+  return int64_t(pt.nstr) * pt.kps + 2 * pt.bonus;
+}
+// Index of the CTA whose range holds linear strip-row L.
+__host__ __device__ __forceinline__ int64_t part_cta_of(const Partials& pt, int64_t L) {
+  if (pt.kps == 0) return cta_of(L, pt.S, pt.G);
+  const int64_t u = L / pt.H, y = L - u * pt.H;
+  const int64_t b = u / pt.nstr, s = u - b * pt.nstr;
+  const int64_t ks = pt.kps + ((s == 0 || s == pt.nstr - 1) ? pt.bonus : 0);
+  const int64_t base = b * part_per_image(pt) + s * pt.kps + (s > 0 ? pt.bonus : 0);
+  return base + ((y + 1) * ks - 1) / pt.H;
+}
+// First strip-row of CTA i (i == G: S).
+__host__ __device__ __forceinline__ int64_t part_start(const Partials& pt, int64_t i) {
+  if (pt.kps == 0) return cta_start(i, pt.S, pt.G);
+  if (i >= pt.G) return pt.S;
+  const int64_t per = part_per_image(pt);
+  const int64_t b = i / per;
+  int64_t r = i - b * per, s, t, ks;
+  if (r < pt.kps + pt.bonus) {
+    s = 0, t = r, ks = pt.kps + pt.bonus;
+  } else {
+    r -= pt.kps + pt.bonus;
+    s = 1 + r / pt.kps;
+    if (s >= pt.nstr - 1) {
+      s = pt.nstr - 1, t = r - int64_t(pt.nstr - 2) * pt.kps, ks = pt.kps + pt.bonus;
+    } else {
+      t = r - (s - 1) * pt.kps, ks = pt.kps;
+    }
+  }
+  return (b * pt.nstr + s) * pt.H + (t * pt.H) / ks;
+}
+
 __device__ __forceinline__ int partial_count(const Partials& pt, int p) {
   if (pt.tiles > 0) return pt.tiles;
   const int64_t img = p / pt.C;
-  const int64_t lo = cta_of(img * pt.U, pt.S, pt.G);
-  const int64_t hi = cta_of((img + 1) * pt.U - 1, pt.S, pt.G);
+  const int64_t lo = part_cta_of(pt, img * pt.U);
+  const int64_t hi = part_cta_of(pt, (img + 1) * pt.U - 1);
   return int(hi - lo + 1);
 }
 

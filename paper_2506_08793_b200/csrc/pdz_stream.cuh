@@ -391,12 +391,12 @@ struct DepSet {
 };
 __device__ __forceinline__ DepSet dep_set(const StreamArgs& a, int L0, int L1, int R) {
   DepSet d;
-  const int S = int(a.pt.S), G = a.pt.G, H = a.H;
+  const int S = int(a.pt.S), H = a.H;
   const int u0 = L0 / H, u1 = (L1 - 1) / H;
   if (u0 != u1) {
     d.n = 3;
-    d.lo[0] = int(cta_of(max(0, L0 - H - R), S, G));
-    d.hi[0] = int(cta_of(min(S - 1, L1 - 1 + H + R), S, G));
+    d.lo[0] = int(part_cta_of(a.pt, max(0, L0 - H - R)));
+    d.hi[0] = int(part_cta_of(a.pt, min(S - 1, L1 - 1 + H + R)));
     d.lo[1] = d.lo[2] = 1;
     d.hi[1] = d.hi[2] = 0;
     return d;
@@ -409,8 +409,8 @@ __device__ __forceinline__ DepSet dep_set(const StreamArgs& a, int L0, int L1, i
     const int s2 = s + i - 1;
     const int base = (b * a.nstrips + s2) * H;
     const bool ok = s2 >= 0 && s2 < a.nstrips;
-    d.lo[i] = ok ? int(cta_of(base + y0, S, G)) : 1;
-    d.hi[i] = ok ? int(cta_of(base + y1 - 1, S, G)) : 0;
+    d.lo[i] = ok ? int(part_cta_of(a.pt, base + y0)) : 1;
+    d.hi[i] = ok ? int(part_cta_of(a.pt, base + y1 - 1)) : 0;
   }
   return d;
 }
@@ -630,8 +630,8 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   const int WP = W + 2 * kPadC;                          // padded iterate row
   const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
   const int S = int(a.pt.S), G = a.pt.G;
-  const int L0 = int(cta_start(blockIdx.x, S, G));
-  const int L1 = int(cta_start(blockIdx.x + 1, S, G));
+  const int L0 = int(part_start(a.pt, blockIdx.x));
+  const int L1 = int(part_start(a.pt, blockIdx.x + 1));
   if (blockIdx.x == a.pt.G) {  // the extra CTA: finaliser
     finalizer_cta(a);
     return;
@@ -661,6 +661,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   // compute thread 0 posts the TMA request for a block's input rows; the
   // service warp issues it once the block's pass is granted
   int req_seq = 0;
+  int slot_img = -1, slot_k = 0;  // partial-sum slot of this CTA in its current image
   auto post = [&](const SBlock& b, int buf) {
     if (tid == 0) {
       ++req_seq;
@@ -886,8 +887,12 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
           t += s_red[w2];
           f |= s_nf[w2];
         }
-        const int k =
-            int(blockIdx.x - cta_of(int64_t(cur.p / a.C) * a.pt.U, S, G));
+        const int img = cur.p / a.C;
+        if (img != slot_img) {  // first CTA of the image: computed once per image
+          slot_img = img;
+          slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(img) * a.pt.U));
+        }
+        const int k = slot_k;
         const size_t slot = (size_t(cur.iter % a.pt.ring) * a.P + cur.p) * a.pt.nbmax + k;
         a.pt.sum[slot] = t;
         a.pt.flag[slot] = f;

@@ -336,6 +336,7 @@ struct Plan {
   int R = 1;
   int tiles_x = 0, tiles_y = 0, nblk = 0;  // tiled
   int G = 0, nstrips = 0;                   // streaming
+  int kps = 0, bonus = 0;                   // per-strip partition (Partials)
   int64_t S = 0, U = 0;
   int nbmax = 0;                            // partial slots per plane
   int pad_r = 0, pad_c = 0;                 // iterate buffer pads (rows, columns)
@@ -410,19 +411,31 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
     const int64_t gmax = int64_t(num_sms()) * occ - 1;  // + 1 finaliser CTA
     const int64_t units = int64_t(P.nstrips) * images;
     int64_t G;
+    P.kps = P.bonus = 0;
     if (units <= gmax) {
+      // per-strip partition: kps CTAs per strip, one more for each border
+      // strip when the budget allows (border rows cost ~15 % more: the
+      // mirrored pad stores), rows split evenly within a strip
       int64_t k = std::max<int64_t>(1, std::min<int64_t>(gmax / units, p->height / 16));
-      if (const char* e = getenv("PDZ_STREAM_K")) k = std::min<int64_t>(k, atoi(e));  // TEMP
-      G = units * k;
+      if (const char* e = getenv("PDZ_STREAM_K")) k = std::min<int64_t>(k, atoi(e));  // tuning
+      int bonus = (P.nstrips >= 2 && images * (int64_t(P.nstrips) * k + 2) <= gmax &&
+                   p->height / (k + 1) >= 16) ? 1 : 0;
+      if (const char* e = getenv("PDZ_STREAM_BONUS")) bonus = bonus && atoi(e) != 0;
+      P.kps = int(k);
+      P.bonus = bonus;
+      G = images * (int64_t(P.nstrips) * k + 2 * bonus);
     } else {
       const int64_t m = (units + gmax - 1) / gmax;  // strips per CTA
       G = (units + m - 1) / m;
     }
     P.G = int(std::max<int64_t>(1, G));
+    Partials q = {};
+    q.S = P.S, q.U = P.U, q.G = P.G, q.kps = P.kps, q.bonus = P.bonus, q.nstr = P.nstrips;
+    q.H = p->height;
     int nb = 1;
-    for (int64_t q = 0; q < images; ++q) {
-      const int64_t lo = cta_of(q * P.U, P.S, P.G);
-      const int64_t hi = cta_of((q + 1) * P.U - 1, P.S, P.G);
+    for (int64_t i = 0; i < images; ++i) {
+      const int64_t lo = part_cta_of(q, i * P.U);
+      const int64_t hi = part_cta_of(q, (i + 1) * P.U - 1);
       nb = std::max<int>(nb, int(hi - lo + 1));
     }
     P.nbmax = nb;
@@ -534,6 +547,10 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   pt.U = pl.U;
   pt.G = pl.G;
   pt.C = pl.stream ? p->channels : 1;
+  pt.kps = pl.kps;
+  pt.bonus = pl.bonus;
+  pt.nstr = pl.nstrips;
+  pt.H = p->height;
   SweepArgs& a = la->tile;
   a.buf0 = buf0;
   a.buf1 = buf1;
