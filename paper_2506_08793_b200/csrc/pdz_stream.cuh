@@ -58,6 +58,10 @@ constexpr int kRPW = 6;                     // output rows per compute warp
 constexpr int kSRB = kSCW * kRPW;           // output rows per block
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
+// The compute thread that does the CTA's serial bookkeeping (posting loads,
+// the Phi / lambda TMA, the partial sums, the progress counter): lane 0 of
+// the last compute warp, whose threads carry one horizontal-pass item fewer.
+constexpr int kLead = kComputeThreads - 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
 // Column pad of the padded iterates: 32 floats (128 B) each side, so padded
 // rows and every strip's first image column are 128-byte aligned (only the
@@ -340,7 +344,7 @@ struct FlatIter {
         fresh = false;
         return kBlock;
       }
-      if (!busy_iter && threadIdx.x == 0)
+      if (!busy_iter && threadIdx.x == kLead)
         st_release_cta_shared(s_progress, pass_index(iter, c, a.C));
       if (++c == a.C) {
         c = 0;
@@ -658,12 +662,12 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   uint32_t phase0 = 0, phase1 = 0, phase_pl = 0;
   int ib = 0;
 
-  // compute thread 0 posts the TMA request for a block's input rows; the
+  // the lead compute thread posts the TMA request for a block's input rows; the
   // service warp issues it once the block's pass is granted
   int req_seq = 0;
   int slot_img = -1, slot_k = 0;  // partial-sum slot of this CTA in its current image
   auto post = [&](const SBlock& b, int buf) {
-    if (tid == 0) {
+    if (tid == kLead) {
       ++req_seq;
       mb.req[req_seq & 1] = LoadReq{b.p, b.x0, b.yb, b.iter, buf, pass_index(b.iter, b.c, a.C)
                                     PDZ_P(, global_ns())};
@@ -678,12 +682,14 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   float acc_nf = 0.0f;
 
   // Per block b (two CTA barriers):
-  //   barrier (block b-1 finished: IN(b-1), H and the Phi / lambda tiles are free)
+  //   (block b-1 ended with a barrier: IN(b-1), H and the Phi / lambda tiles
+  //   are free)
   //   -> post IN(b+1) (the service warp loads it once granted, overlapping
   //      block b) and queue the Phi / lambda tiles of b (hidden by the H pass)
   //   -> wait IN(b); blur its n + 2R rows into H
   //   -> barrier; wait Phi / lambda
-  //   -> vertical pass + divergence + update.
+  //   -> vertical pass + divergence + update
+  //   -> barrier; flush the plane partial / publish the pass.
   while (have) {
     PDZ_P(const long long tn_ = global_ns();)
     const int nk = it.next(a, nxt, cur.iter, &mb.progress, &mb.fin);
@@ -696,10 +702,11 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     const bool col_ok = gx < W;
     float* __restrict__ uout_all = (cur.iter & 1) ? a.buf1 : a.buf0;
 
-    PDZ_PT(2, compute_bar());
+    // (the previous block ended with a CTA barrier: IN(b-1), H and the
+    // Phi / lambda tiles are free)
     PDZ_P(pf[6] += 1;)
     if (have_nxt) post(nxt, ib ^ 1);
-    if (tid == 0) {  // Phi / lambda tiles of this block (iteration invariant)
+    if (tid == kLead) {  // Phi / lambda tiles of this block (iteration invariant)
       mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
       tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
       tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
@@ -871,15 +878,21 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     PDZ_P(pf[10] += global_ns() - tph;)
     // ---- flush the plane partial when the plane changes; publish the pass
     const bool pass_end = !have_nxt || nxt.pass_start;
-    if (pass_end || nxt.p != cur.p) {
+    const bool flush = pass_end || nxt.p != cur.p;
+    if (flush) {
       double s = warp_sum(acc_r2);
       const int nfw = __any_sync(0xffffffffu, !(acc_nf == 0.0f));
       if (lane == 0) {
         s_red[warp] = s;
         s_nf[warp] = nfw;
       }
-      PDZ_PT(5, compute_bar());  // also orders every output store of the pass before the flag
-      if (tid == 0) {
+    }
+    // end of the block: every read of IN / H / Phi / lambda and every output
+    // store of the block precede this barrier (it also orders the pass's
+    // outputs before the progress flag)
+    PDZ_PT(5, compute_bar());
+    if (flush) {
+      if (tid == kLead) {
         double t = 0.0;
         int f = 0;
 #pragma unroll
@@ -916,7 +929,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     have = have_nxt;
     ib ^= 1;
   }
-  if (tid == 0) {
+  if (tid == kLead) {
     st_release_cta_shared(&mb.progress, pass_index(a.iter_last, a.C - 1, a.C));
     st_release_cta_shared(&mb.exit, 1);
     PDZ_P(if (a.prof) {
