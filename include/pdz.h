@@ -247,6 +247,24 @@ float pdz_last_sweep_kernel_ms(void);
 int32_t pdz_clamp_interleave(const float* planes, int32_t height, int32_t width,
                              int32_t channels, void* out, int32_t out_is_f64, void* stream);
 
+/* ---- image I/O and evaluation ------------------------ */
+/* save_image quantisation (image.py:128-145): out[i] = floor(clamp(v, 0, 1) *
+ * 255 + 0.5) in float64 for n samples; *flag = 1 if any sample is non-finite
+ * (clamp01 rejects those, image.py:56-61).  flag is a device int32. */
+int32_t pdz_quantize_u8(const double* image, int64_t n, uint8_t* out, int32_t* flag,
+                        void* stream);
+/* synthesize_haze (scattering.py:142-158): out = J * t + A * (1 - t) in
+ * float64, J interleaved (pixels, channels), t (pixels), A (channels). */
+int32_t pdz_synthesize_haze(const double* clean, const double* transmission,
+                            const double* airlight, int64_t pixels, int32_t channels,
+                            double* out, void* stream);
+/* metrics.compare (metrics.py:20-37): sums[0] = sum (x - y)^2, sums[1] =
+ * sum |x - y| over n samples (fixed-order fp64 reduction); *flag bit 1 / 2:
+ * first / second image has a value outside [0, 1] or non-finite. */
+size_t pdz_compare_workspace_bytes(void);
+int32_t pdz_compare(const double* x, const double* y, int64_t n, double* sums, int32_t* flag,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

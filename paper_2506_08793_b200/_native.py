@@ -101,6 +101,10 @@ _SIGNATURES = {
     "pdz_solve_kernel_launches": (_i64, [_pp]),
     "pdz_sweep_kernel_kind": (_i32, [_pp]),
     "pdz_clamp_interleave": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "pdz_quantize_u8": (_i32, [_vp, ctypes.c_int64, _vp, _vp, _vp]),
+    "pdz_synthesize_haze": (_i32, [_vp, _vp, _vp, ctypes.c_int64, _i32, _vp, _vp]),
+    "pdz_compare_workspace_bytes": (_sz, []),
+    "pdz_compare": (_i32, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _sz, _vp]),
     "pdz_guided_workspace_bytes": (_sz, [_i32, _i32]),
     "pdz_box_mean": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
     "pdz_guided_filter": (_i32, [_vp, _vp, _i32, _i32, _i32, _f64, _vp, _vp, _sz, _vp]),

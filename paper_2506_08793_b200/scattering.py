@@ -23,6 +23,7 @@ __all__ = [
     "estimate_atmospheric_light_indices",
     "estimate_transmission",
     "reconstruct",
+    "synthesize_haze",
 ]
 
 
@@ -222,3 +223,27 @@ def reconstruct(image, transmission, airlight, t_floor: float = 0.1):
 
 def _count(h: int, w: int, fraction: float) -> int:
     return math.ceil(fraction * h * w)
+
+
+def synthesize_haze(clean, transmission, airlight):
+    """Forward haze model J * t + A * (1 - t) (scattering.py:142-158), in
+    float64 on the device with the reference's operation order (bitwise)."""
+    import torch
+
+    img = validate_image(clean)
+    _unit_range(img)
+    t = validate_field(transmission)
+    if tuple(t.shape) != tuple(img.shape[:2]):
+        raise ValueError(f"transmission shape {tuple(t.shape)} != image shape "
+                         f"{tuple(img.shape[:2])}")
+    if float(t.min()) < 0.0 or float(t.max()) > 1.0:
+        raise ValueError("transmission values must lie in [0, 1]")
+    h, w, c = img.shape
+    a = _airlight_vector(airlight, c)
+    img_dev = to_device(img, torch.float64)
+    t_dev = to_device(t, torch.float64)
+    a_dev = _device_vec(a)
+    out = torch.empty_like(img_dev)
+    nat.check(nat.lib().pdz_synthesize_haze(nat.ptr(img_dev), nat.ptr(t_dev), nat.ptr(a_dev),
+                                            h * w, c, nat.ptr(out), nat.stream_ptr()))
+    return to_host(out, clean)

@@ -20,6 +20,8 @@ Fixtures
                    checked here against demos/out/residual_traces.csv
   config1.npz      BASELINE config 1 (256x256x3, patch 15, sigma 2 / K 13,
                    50 iterations, tau = TAU_STABLE) through dehaze
+  cli.npz          the reference command line (synthesize / dehaze / evaluate)
+                   on small Netpbm files: input and output bytes
 """
 
 from __future__ import annotations
@@ -240,7 +242,67 @@ def config1():
         tau_bound=np.array([tr.tau_bound for tr in info.traces]))
 
 
+def cli():
+    """The reference command line (cli.py) end to end on small Netpbm files:
+    synthesize / dehaze (stable tau, default pipeline; no-pde; grayscale) /
+    evaluate, plus a commented-header P6 through load_image."""
+    import contextlib
+    import io
+    import tempfile
+
+    from pdehaze.cli import main as ref_main
+    from pdehaze.image import load_image as ref_load
+    from pdehaze.image import save_image as ref_save
+
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        def path(name):
+            return os.path.join(d, name)
+
+        def read(name):
+            with open(path(name), "rb") as fh:
+                return np.frombuffer(fh.read(), dtype=np.uint8).copy()
+
+        scene = make_hazy_scene(48, 64, 3, 0)
+        ref_save(scene.clear.astype(np.float64), path("clean.ppm"))
+        rng = np.random.default_rng(77)
+        ref_save(rng.uniform(0.2, 0.95, size=(48, 64)), path("tmap.pgm"))
+        ref_save(scene.clear.astype(np.float64)[:, :, 1], path("gray.pgm"))
+        runs = {
+            "synth": ["synthesize", path("clean.ppm"), path("hazy.ppm"), "--t", "0.4",
+                      "--airlight", "0.8,0.85,0.9"],
+            "synth_map": ["synthesize", path("clean.ppm"), path("hazy_map.ppm"), "--t-map",
+                          path("tmap.pgm"), "--airlight", "0.9"],
+            "dehaze": ["dehaze", path("hazy.ppm"), path("dehazed.ppm"), "--tau", repr(TAU_STABLE),
+                       "--max-iters", "30", "--rel-tol", "1e-300", "--trace", path("trace.csv")],
+            "nopde": ["dehaze", path("hazy.ppm"), path("nopde.ppm"), "--tau", repr(TAU_STABLE),
+                      "--ablate", "no-pde"],
+            "gray": ["dehaze", path("gray.pgm"), path("gray_out.pgm"), "--tau", repr(TAU_STABLE),
+                     "--max-iters", "20", "--rel-tol", "1e-300", "--ablate", "no-guided"],
+        }
+        for key in ("synth", "synth_map", "dehaze", "nopde", "gray"):
+            assert ref_main(runs[key]) == 0, key
+        for name in ("clean.ppm", "tmap.pgm", "gray.pgm", "hazy.ppm", "hazy_map.ppm",
+                     "dehazed.ppm", "nopde.ppm", "gray_out.pgm"):
+            out["file_" + name.replace(".", "_")] = read(name)
+        with open(path("trace.csv")) as fh:
+            out["trace_csv"] = np.array(fh.read())
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert ref_main(["evaluate", path("clean.ppm"), path("hazy.ppm")]) == 0
+        out["evaluate_json"] = np.array(buf.getvalue().strip())
+        # commented header, CRLF-free, comment between every field
+        payload = rng.integers(0, 256, size=(5, 7, 3), dtype=np.uint8)
+        with open(path("commented.ppm"), "wb") as fh:
+            fh.write(b"P6 # magic\n# a comment line\n7 # width\n5\n# maxval next\n255\n")
+            fh.write(payload.tobytes())
+        out["file_commented_ppm"] = read("commented.ppm")
+        out["commented_values"] = ref_load(path("commented.ppm"))
+    np.savez_compressed(os.path.join(HERE, "cli.npz"), **out)
+
+
 if __name__ == "__main__":
+    cli()
     operators()
     frontend()
     solve()
