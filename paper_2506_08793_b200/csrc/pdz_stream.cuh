@@ -243,9 +243,11 @@ struct SBlock {
 struct RangeIter {
   int L, L0, L1, b, s, y;
   int b0, s0, y0;
+  bool check_stop;  // some plane has stopped: look up frozen planes (uniform per pass)
   __device__ __forceinline__ void init(int l0, int l1, const StreamArgs& a) {
     L = L0 = l0;
     L1 = l1;
+    check_stop = false;
     const int u = l0 / a.H;
     y0 = l0 - u * a.H;
     b0 = u / a.nstrips;
@@ -265,11 +267,12 @@ struct RangeIter {
       ++b;
     }
   }
+  template <bool STOP>
   __device__ __forceinline__ bool next(const StreamArgs& a, int iter, int c, SBlock& blk) {
     while (L < L1) {
       const int seg_end = min(L1, L - y + a.H);
       const int p = b * a.C + c;
-      if (a.stop_rule && a.st.stop_iter) {
+      if (STOP && check_stop) {
         const int st = a.st.stop_iter[p];
         if (st != 0 && st < iter - 1) {
           L = seg_end;
@@ -321,23 +324,29 @@ struct FlatIter {
   bool fresh;  // next block starts a new pass
   bool ended;
   PDZ_P(long long grant_ns;)
+  template <bool STOP>
   __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy_iter,
-                                      int* s_progress, const int* s_fin) {
+                                      int* s_progress, const int* s_fin, const int* s_anystop) {
     while (!ended && iter <= a.iter_last) {
-      if (fresh && a.stop_rule && a.st.stop_iter && iter > 2) {
+      if (STOP && fresh && a.st.stop_iter && iter > 2) {
         if (busy_iter && iter - 2 >= busy_iter) return kDefer;
         PDZ_P(const long long tg = global_ns();)
         wait_shared_ge(s_fin, iter - 2);
         PDZ_P(grant_ns += global_ns() - tg;)
-        // the all-stopped iteration is published before fin reaches it, so
-        // this test is uniform across threads
-        const int all = ld_relaxed(a.flags);
-        if (all != 0 && all <= iter - 2) {
-          ended = true;
-          break;
+        // Only once some plane has stopped are the global stop records
+        // consulted (no dependent global load on the per-block path before
+        // that).  A stop at iteration <= iter - 2 is mirrored before fin
+        // reaches it, so both tests are uniform across threads.
+        r.check_stop = ld_acquire_cta_shared(s_anystop) != 0;
+        if (r.check_stop) {
+          const int all = ld_relaxed(a.flags);
+          if (all != 0 && all <= iter - 2) {
+            ended = true;
+            break;
+          }
         }
       }
-      if (r.next(a, iter, c, blk)) {
+      if (r.template next<STOP>(a, iter, c, blk)) {
         blk.iter = iter;
         blk.c = c;
         blk.pass_start = fresh;
@@ -430,6 +439,7 @@ struct Mailbox {
   int fin;       // mirror of the global `fin` (service warp)
   int req_seq;   // TMA requests posted (compute thread 0)
   LoadReq req[2];  // request s in req[s & 1]: at most two outstanding (IN(b), IN(b+1))
+  int anystop;   // some plane has stopped (service warp; released before `fin`)
 };
 
 // Warp kSCW runs every gpu-scope synchronisation of its CTA, so compute warps
@@ -443,14 +453,15 @@ struct Mailbox {
 //    (n-1, c), partial slot n % kRing is free (fin >= n - kRing) and, with the
 //    stop rule, fin >= n - 2 (once every plane has stopped, anything goes);
 //  * fin: with the stop rule, the global `fin` is mirrored for the iterator.
-template <int R>
+template <int R, bool STOP>
 __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float* in1,
                              uint64_t* bars, const DepSet& dep) {
   const int lane = threadIdx.x & 31;
   const int C = a.C;
   const bool fin_on = a.st.stop_iter != nullptr;
-  const bool mirror_fin = fin_on && a.stop_rule;
+  const bool mirror_fin = fin_on && STOP;
   int published = 0, granted = 0, issued = 0, fin_seen = 0;
+  bool anystop = false;
   long long t0 = global_ns();
   PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
   PDZ_P(long long t_need = 0;)
@@ -475,7 +486,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       }
       PDZ_P(const bool ok_dep = __all_sync(0xffffffffu, ok);)
       if (lane == 0 && fin_on) {
-        const int need_fin = a.stop_rule ? n - 2 : n - kRing;
+        const int need_fin = STOP ? n - 2 : n - kRing;
         if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
       }
       grant = __all_sync(0xffffffffu, ok);
@@ -494,6 +505,10 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       }
       if (f > fin_seen) {
         fin_seen = f;
+        if (!anystop && a.st.running[0] < a.P) {  // written before fin (finaliser)
+          anystop = true;
+          if (lane == 0) st_release_cta_shared(&mb->anystop, 1);
+        }
         if (lane == 0) st_release_cta_shared(&mb->fin, f);
       }
       if (grant) {
@@ -600,7 +615,7 @@ __device__ void finalizer_cta(const StreamArgs& a) {
 }
 
 // ------------------------------------------------------------- kernel --
-template <int R, bool EDGE>
+template <int R, bool EDGE, bool STOP>  // STOP: the relative-change stop rule is armed
 __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     stream_kernel(const __grid_constant__ StreamArgs a) {
   using Gm = SGeo<R>;
@@ -625,6 +640,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     mb.progress = 0;
     mb.exit = 0;
     mb.fin = 0;
+    mb.anystop = 0;
     mb.req_seq = 0;
   }
   __syncthreads();
@@ -641,7 +657,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     return;
   }
   if (warp == kSCW) {
-    service_loop<R>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R));
+    service_loop<R, STOP>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R));
     return;
   }
 
@@ -676,7 +692,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   };
 
   SBlock cur, nxt;
-  bool have = it.next(a, cur, 0, &mb.progress, &mb.fin) == kBlock;
+  bool have = it.template next<STOP>(a, cur, 0, &mb.progress, &mb.fin, &mb.anystop) == kBlock;
   if (have) post(cur, 0);
   double acc_r2 = 0.0;
   float acc_nf = 0.0f;
@@ -692,7 +708,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   //   -> barrier; flush the plane partial / publish the pass.
   while (have) {
     PDZ_P(const long long tn_ = global_ns();)
-    const int nk = it.next(a, nxt, cur.iter, &mb.progress, &mb.fin);
+    const int nk = it.template next<STOP>(a, nxt, cur.iter, &mb.progress, &mb.fin, &mb.anystop);
     PDZ_P(pf[12] += global_ns() - tn_;)
     bool have_nxt = nk == kBlock;
     float* const in_cur = ib ? in1 : in0;
@@ -922,7 +938,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       PDZ_P(pf[7] += 1;)
       // the next pass needs this CTA's own progress: published above (the
       // flush barrier ordered every store of the pass); continue when idle
-      have_nxt = it.next(a, nxt, 0, &mb.progress, &mb.fin) == kBlock;
+      have_nxt = it.template next<STOP>(a, nxt, 0, &mb.progress, &mb.fin, &mb.anystop) == kBlock;
       if (have_nxt) post(nxt, ib ^ 1);
     }
     cur = nxt;
@@ -943,30 +959,34 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
 // ------------------------------------------------------------------- host --
 using StreamFn = void (*)(const StreamArgs);
 
-template <int R, bool EDGE>
+template <int R, bool EDGE, bool STOP>
 static StreamFn stream_prepared(size_t* smem) {
   static_assert(SGeo<R>::FITS, "staging buffers exceed shared memory");
   static bool done = false;
   *smem = SGeo<R>::SMEM;
   if (!done) {
-    cudaFuncSetAttribute(stream_kernel<R, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(stream_kernel<R, EDGE, STOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(SGeo<R>::SMEM));
     done = true;
   }
-  return stream_kernel<R, EDGE>;
+  return stream_kernel<R, EDGE, STOP>;
 }
 
-template <bool EDGE>
-static StreamFn stream_pick(int R, size_t* smem) {
+template <bool EDGE, bool STOP>
+static StreamFn stream_pick_stop(int R, size_t* smem) {
   switch (R) {  // radii whose staging fits in shared memory (SGeo<R>::FITS)
-    case 1: return stream_prepared<1, EDGE>(smem);
-    case 2: return stream_prepared<2, EDGE>(smem);
-    case 3: return stream_prepared<3, EDGE>(smem);
-    case 6: return stream_prepared<6, EDGE>(smem);
-    case 9: return stream_prepared<9, EDGE>(smem);
-    case 12: return stream_prepared<12, EDGE>(smem);
+    case 1: return stream_prepared<1, EDGE, STOP>(smem);
+    case 2: return stream_prepared<2, EDGE, STOP>(smem);
+    case 3: return stream_prepared<3, EDGE, STOP>(smem);
+    case 6: return stream_prepared<6, EDGE, STOP>(smem);
+    case 9: return stream_prepared<9, EDGE, STOP>(smem);
+    case 12: return stream_prepared<12, EDGE, STOP>(smem);
     default: return nullptr;
   }
+}
+template <bool EDGE>
+static StreamFn stream_pick(int R, bool stop, size_t* smem) {
+  return stop ? stream_pick_stop<EDGE, true>(R, smem) : stream_pick_stop<EDGE, false>(R, smem);
 }
 
 }  // namespace pdz

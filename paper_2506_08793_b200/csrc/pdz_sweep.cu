@@ -381,7 +381,8 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
   if (allow_stream && !g_force_tiled && p->width % 4 == 0 && p->height >= 2 * P.R &&
       p->width >= 2 * rp &&
       strip_rows + p->height < (int64_t(1) << 31))
-    sfn = edge ? stream_pick<true>(P.R, &smem) : stream_pick<false>(P.R, &smem);
+    sfn = edge ? stream_pick<true>(P.R, p->rel_tol >= 0.0, &smem)
+               : stream_pick<false>(P.R, p->rel_tol >= 0.0, &smem);
   int occ = 0;
   if (sfn) {
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);

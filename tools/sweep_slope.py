@@ -25,18 +25,32 @@ for iters in (25, 50, 100, 200, 400):
     phi, lam = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg))
     prm = _params(size, size, 3, 3, cfg)
     ws = torch.empty(lib.pdz_solve_workspace_bytes(prm), dtype=torch.uint8, device="cuda")
+    stop = os.environ.get("STOPRULE") == "1"  # fixed_point_solve path: stop rule armed
+    import numpy as np
+    out = torch.empty_like(phi)
+    hn = np.zeros((iters, 3)); hi = np.zeros(3, np.int32)
+    hc = np.zeros(3, np.int32); hf = np.zeros(3, np.int32)
+
+    def run():
+        if stop:
+            nat.check(lib.pdz_fixed_point_solve(prm, nat.ptr(phi), nat.ptr(lam), nat.ptr(out),
+                                                hn.ctypes.data, hi.ctypes.data, hc.ctypes.data,
+                                                hf.ctypes.data, nat.ptr(ws), ws.numel(),
+                                                nat.stream_ptr()))
+        else:
+            nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(phi), nat.ptr(lam),
+                                                       nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+
     for _ in range(3):
-        nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(phi), nat.ptr(lam), nat.ptr(ws),
-                                                   ws.numel(), nat.stream_ptr()))
+        run()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    lib.pdz_time_sweep_kernels(1)
+    ms = 0.0
     for _ in range(5):
-        nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(phi), nat.ptr(lam), nat.ptr(ws),
-                                                   ws.numel(), nat.stream_ptr()))
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 5
+        run()
+        torch.cuda.synchronize()
+        ms += lib.pdz_last_sweep_kernel_ms() / 5
+    lib.pdz_time_sweep_kernels(0)
     res.append((iters, ms))
     print(f"iters {iters:4d}: {ms*1e3:9.1f} us  ({ms*1e3/iters:6.2f} us/sweep)  kind "
           f"{lib.pdz_sweep_kernel_kind(prm)}", flush=True)
