@@ -232,6 +232,38 @@ __device__ __forceinline__ float sflux(float jump, float along, float eps) {
   return jump * rcp_approx(sqrt_approx(s) + eps);
 }
 
+// Packed float pairs (FADD2 / FMUL2): per-lane IEEE round-to-nearest, so a
+// packed op is bitwise the two scalar ops.
+__device__ __forceinline__ unsigned long long f2bits(float2 a) {
+  return *reinterpret_cast<unsigned long long*>(&a);
+}
+__device__ __forceinline__ float2 bits2f(unsigned long long d) {
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2bits(a)), "l"(f2bits(b)));
+  return bits2f(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2bits(a)), "l"(f2bits(b)));
+  return bits2f(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2bits(a)), "l"(f2bits(b)));
+  return bits2f(d);
+}
+// sflux on a pair of faces (same per-lane arithmetic as sflux).
+template <bool EDGE>
+__device__ __forceinline__ float2 sflux2(float2 jump, float2 along, float2 eps2) {
+  if (!EDGE) return jump;
+  const float2 s = ffma2(jump, jump, mul2(along, along));
+  const float2 q = add2(make_float2(sqrt_approx(s.x), sqrt_approx(s.y)), eps2);
+  return mul2(jump, make_float2(rcp_approx(q.x), rcp_approx(q.y)));
+}
+
 // ----------------------------------------------------------- iteration --
 struct SBlock {
   int p, x0, yb, n;         // plane, strip origin, first row, rows
@@ -800,17 +832,18 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       const float* urow = in_cur + (R + j0 - 1) * Gm::PITCH + Gm::RP + c;
       const float sx0 = (gx == 0) ? 1.0f : 0.5f;          // column c   (c >= 0)
       const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;  // column c+1
-      float lA = urow[-1], rA = urow[2];
+      const float2 half2 = make_float2(0.5f, 0.5f), eps2 = make_float2(a.eps, a.eps);
+      float2 eA = make_float2(urow[-1], urow[2]);
       float2 cA = *reinterpret_cast<const float2*>(urow);
       urow += Gm::PITCH;
-      float lB = urow[-1], rB = urow[2];
+      float2 eB = make_float2(urow[-1], urow[2]);
       float2 cB = *reinterpret_cast<const float2*>(urow);
-      float2 xA = make_float2(sx0 * (cA.y - lA), sx1 * (rA - cA.x));
-      float2 xB = make_float2(sx0 * (cB.y - lB), sx1 * (rB - cB.x));
+      float2 xA = make_float2(sx0 * (cA.y - eA.x), sx1 * (eA.y - cA.x));
+      float2 xB = make_float2(sx0 * (cB.y - eB.x), sx1 * (eB.y - cB.x));
       // south flux of the row above the first output row
-      float2 fs_up = make_float2(sflux<EDGE>(cB.x - cA.x, 0.5f * (xA.x + xB.x), a.eps),
-                                 sflux<EDGE>(cB.y - cA.y, 0.5f * (xA.y + xB.y), a.eps));
-      float r2 = 0.f;
+      float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(half2, add2(xA, xB)), eps2);
+      float2 r2p = make_float2(0.f, 0.f), nfp = make_float2(0.f, 0.f);
+      const float2 zero2 = make_float2(0.f, 0.f), tau2 = make_float2(a.tau, a.tau);
       float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + kPadC;
       // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
       // the reversed column pair at column xm; rows j < jt also go to row
@@ -832,39 +865,39 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         float* const bot = uout + ptrdiff_t(2 * H - 1 - y0) * WP + gx;  // row 2H-1-y
 #pragma unroll
         for (int j = 0; j < kRPW; ++j) {
+          // Column pairs in packed float2: c = (u[c], u[c+1]), e = (u[c-1], u[c+2]).
           urow += Gm::PITCH;
-          const float lC = urow[-1], rC = urow[2];
+          const float2 eC = make_float2(urow[-1], urow[2]);
           const float2 cC = *reinterpret_cast<const float2*>(urow);
-          const float2 xC = make_float2(sx0 * (cC.y - lC), sx1 * (rC - cC.x));
+          const float2 xC = make_float2(sx0 * (cC.y - eC.x), sx1 * (eC.y - cC.x));
           const float sy = (j == jz0 || j == jz1) ? 1.0f : 0.5f;
-          // centred vertical differences at columns c-1, c, c+1, c+2
-          const float dl = sy * (lC - lA);
-          const float d0 = sy * (cC.x - cA.x);
-          const float d1 = sy * (cC.y - cA.y);
-          const float dr = sy * (rC - rA);
+          const float2 sy2 = make_float2(sy, sy);
+          // centred vertical differences: d = columns (c, c+1), de = (c-1, c+2)
+          const float2 d = mul2(sy2, sub2(cC, cA));
+          const float2 de = mul2(sy2, sub2(eC, eA));
           const float u0 = cB.x, u1 = cB.y;
-          const float fw = sflux<EDGE>(u0 - lB, 0.5f * (dl + d0), a.eps);  // face c-1|c
-          const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d0 + d1), a.eps);  // face c|c+1
-          const float fe = sflux<EDGE>(rB - u1, 0.5f * (d1 + dr), a.eps);  // face c+1|c+2
-          const float2 fs_dn = make_float2(sflux<EDGE>(cC.x - u0, 0.5f * (xB.x + xC.x), a.eps),
-                                           sflux<EDGE>(cC.y - u1, 0.5f * (xB.y + xC.y), a.eps));
-          const float div0 = ((fm - fw) + fs_dn.x) - fs_up.x;
-          const float div1 = ((fe - fm) + fs_dn.y) - fs_up.y;
+          // east faces c-1|c and c+1|c+2 as one pair: the second with its jump
+          // negated, (u0 - l, u1 - r) = cB - eB; sflux is odd in the jump, so
+          // the pair is (fw, -fe) exactly
+          const float2 fwe = sflux2<EDGE>(sub2(cB, eB), mul2(half2, add2(de, d)), eps2);
+          const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d.x + d.y), a.eps);  // face c|c+1
+          const float2 fs_dn = sflux2<EDGE>(sub2(cC, cB), mul2(half2, add2(xB, xC)), eps2);
+          // div0 = ((fm - fw) + s0) - n0, div1 = ((fe - fm) + s1) - n1, with
+          // fe - fm = -(fm + (-fe)) exactly
+          const float2 div = sub2(add2(make_float2(fm - fwe.x, -(fm + fwe.y)), fs_dn), fs_up);
+          const float2 cB_old = cB;
           fs_up = fs_dn;
-          lA = lB;
-          rA = rB;
+          eA = eB;
           cA = cB;
           xA = xB;
-          lB = lC;
-          rB = rC;
+          eB = eC;
           cB = cC;
           xB = xC;
           const float2 phv = *reinterpret_cast<const float2*>(pl_row + j * kSTW);
           const float2 lmv = *reinterpret_cast<const float2*>(lm_row + j * kSTW);
-          const float r0 = fmaf(-lmv.x, G2[j].x, div0) + phv.x;
-          const float r1 = fmaf(-lmv.y, G2[j].y, div1) + phv.y;
-          const float n0 = fmaf(a.tau, r0, u0);
-          const float n1 = fmaf(a.tau, r1, u1);
+          const float2 rr = add2(ffma2(make_float2(-lmv.x, -lmv.y), G2[j], div), phv);
+          const float2 nn = ffma2(tau2, rr, cB_old);
+          const float r0 = rr.x, r1 = rr.y, n0 = nn.x, n1 = nn.y;
           if (j < nrows) {
             *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
             if (MIR) {
@@ -878,8 +911,8 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
               }
 #endif
             }
-            r2 = fmaf(r0, r0, fmaf(r1, r1, r2));
-            acc_nf = fmaf(n0, 0.0f, fmaf(n1, 0.0f, acc_nf));  // NaN iff non-finite update
+            r2p = ffma2(rr, rr, r2p);
+            nfp = ffma2(nn, zero2, nfp);  // NaN iff non-finite update
           }
           orow += WP;
         }
@@ -888,7 +921,8 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         rows(std::true_type{});
       else
         rows(std::false_type{});
-      acc_r2 += double(r2);
+      acc_r2 += double(r2p.x + r2p.y);
+      acc_nf += nfp.x + nfp.y;
     }
 
     PDZ_P(pf[10] += global_ns() - tph;)
