@@ -269,16 +269,37 @@ __global__ void select_count_kernel(const double* __restrict__ dark, int64_t n,
 }
 
 // Exclusive scans of the per-block counts (single block, sequential chunks).
+// Exclusive scan of the per-block counts, one block of 1024 threads: each
+// thread scans a contiguous run, then the run totals are scanned across the
+// block (integer sums: any order is exact).
 __global__ void select_scan_kernel(unsigned int* gt_cnt, unsigned int* eq_cnt, int nblocks) {
-  if (threadIdx.x == 0) {
-    unsigned int a = 0, b = 0;
-    for (int i = 0; i < nblocks; ++i) {
-      const unsigned int x = gt_cnt[i], y = eq_cnt[i];
-      gt_cnt[i] = a;
-      eq_cnt[i] = b;
-      a += x;
-      b += y;
-    }
+  __shared__ unsigned int sg[1024], se[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (nblocks + nt - 1) / nt;
+  const int lo = min(nblocks, t * per), hi = min(nblocks, lo + per);
+  unsigned int a = 0, b = 0;
+  for (int i = lo; i < hi; ++i) {
+    a += gt_cnt[i];
+    b += eq_cnt[i];
+  }
+  sg[t] = a;
+  se[t] = b;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {  // Hillis-Steele inclusive scan
+    const unsigned int xa = t >= o ? sg[t - o] : 0u, xb = t >= o ? se[t - o] : 0u;
+    __syncthreads();
+    sg[t] += xa;
+    se[t] += xb;
+    __syncthreads();
+  }
+  a = sg[t] - a;  // exclusive start of this thread's run
+  b = se[t] - b;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned int x = gt_cnt[i], y = eq_cnt[i];
+    gt_cnt[i] = a;
+    eq_cnt[i] = b;
+    a += x;
+    b += y;
   }
 }
 
@@ -343,12 +364,16 @@ __global__ void select_compact_kernel(const double* __restrict__ dark, int64_t n
 
 // Rank of each candidate under (key desc, index asc) by counting; keys are
 // unique once the index breaks ties, so ranks form a permutation.
+// Rank sort of the m candidates by (key desc, index asc): 4 threads per
+// candidate (adjacent lanes) each count a quarter of the comparisons; 64
+// candidates per block of 256 threads.
 __global__ void select_rank_kernel(const unsigned long long* __restrict__ cand_key,
                                    const int64_t* __restrict__ cand_idx, int64_t m,
                                    int64_t* __restrict__ sorted_idx) {
   __shared__ unsigned long long sk[256];
   __shared__ int64_t si[256];
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int q = threadIdx.x & 3;
+  const int64_t i = int64_t(blockIdx.x) * 64 + (threadIdx.x >> 2);
   const unsigned long long ki = i < m ? cand_key[i] : 0ull;
   const int64_t ii = i < m ? cand_idx[i] : 0;
   int64_t rank = 0;
@@ -360,12 +385,14 @@ __global__ void select_rank_kernel(const unsigned long long* __restrict__ cand_k
     }
     __syncthreads();
     const int lim = int(m - j0 < 256 ? m - j0 : 256);
-    for (int j = 0; j < lim; ++j) {
+    for (int j = q; j < lim; j += 4) {
       const unsigned long long kj = sk[j];
       rank += (kj > ki) || (kj == ki && si[j] < ii);
     }
   }
-  if (i < m) sorted_idx[rank] = ii;
+  rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+  rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+  if (i < m && q == 0) sorted_idx[rank] = ii;
 }
 
 // A = mean of I over the selection, clipped to [0.05, 1] (scattering.py:106-107).
@@ -407,27 +434,31 @@ __device__ double pairwise_sum_dev(const double* a, int64_t n) {
   return __dadd_rn(pairwise_sum_dev(a, half), pairwise_sum_dev(a + half, n - half));
 }
 
+// One block per channel; the sequential sum (C = 3) reads the values from
+// shared memory, staged in chunks by the whole block (the order is kept).
 __global__ void airlight_mean_kernel(const double* __restrict__ vals, int C, int64_t m,
                                      double* __restrict__ airlight) {
-  const int c = threadIdx.x;
-  if (c >= C) return;
+  constexpr int kChunk = 2048;
+  __shared__ double sv[kChunk];
+  const int c = blockIdx.x;
   const double* v = vals + size_t(c) * m;
   double s = 0.0;
   if (C == 1) {
-    s = __dadd_rn(0.0, pairwise_sum_dev(v, m));
+    if (threadIdx.x == 0) s = __dadd_rn(0.0, pairwise_sum_dev(v, m));
   } else {
-    int64_t j = 0;
-    for (; j + 8 <= m; j += 8) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = v[j + k];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, x[k]);
+    for (int64_t j0 = 0; j0 < m; j0 += kChunk) {
+      const int cnt = int(m - j0 < kChunk ? m - j0 : kChunk);
+      __syncthreads();
+      for (int k = threadIdx.x; k < cnt; k += blockDim.x) sv[k] = v[j0 + k];
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int k = 0; k < cnt; ++k) s = __dadd_rn(s, sv[k]);
     }
-    for (; j < m; ++j) s = __dadd_rn(s, v[j]);
   }
-  const double mean = __ddiv_rn(s, double(m));
-  airlight[c] = fmin(fmax(mean, 0.05), 1.0);
+  if (threadIdx.x == 0) {
+    const double mean = __ddiv_rn(s, double(m));
+    airlight[c] = fmin(fmax(mean, 0.05), 1.0);
+  }
 }
 
 static int64_t airlight_count(int H, int W, double fraction) {
@@ -628,17 +659,17 @@ int32_t pdz_atmospheric_light(const void* image, int32_t image_is_f64, int32_t h
   PDZ_CHECK_LAUNCH("radix select");
   const int nb = int((n + kSelBlock - 1) / kSelBlock);
   select_count_kernel<<<nb, kSelThreads, 0, s>>>(dark, n, L.st, L.gt, L.eq);
-  select_scan_kernel<<<1, 32, 0, s>>>(L.gt, L.eq, nb);
+  select_scan_kernel<<<1, 1024, 0, s>>>(L.gt, L.eq, nb);
   select_compact_kernel<<<nb, kSelThreads, 0, s>>>(dark, n, L.st, L.gt, L.eq,
                                                    (unsigned long long)m, L.ckey, L.cidx);
-  select_rank_kernel<<<int((m + 255) / 256), 256, 0, s>>>(L.ckey, L.cidx, m, L.sorted);
+  select_rank_kernel<<<int((m + 63) / 64), 256, 0, s>>>(L.ckey, L.cidx, m, L.sorted);
   if (image_is_f64)
     airlight_gather_kernel<double><<<grid_for(m), 256, 0, s>>>(image, channels, L.sorted, m,
                                                                L.vals);
   else
     airlight_gather_kernel<float><<<grid_for(m), 256, 0, s>>>(image, channels, L.sorted, m,
                                                               L.vals);
-  airlight_mean_kernel<<<1, 32, 0, s>>>(L.vals, channels, m, airlight);
+  airlight_mean_kernel<<<channels, 256, 0, s>>>(L.vals, channels, m, airlight);
   PDZ_CHECK_LAUNCH("airlight");
   if (picked)
     PDZ_CUDA(cudaMemcpyAsync(picked, L.sorted, size_t(m) * 8, cudaMemcpyDeviceToDevice, s),

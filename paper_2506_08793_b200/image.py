@@ -10,8 +10,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["validate_image", "validate_field", "clamp01", "is_device_array", "to_device",
-           "to_host"]
+__all__ = ["validate_image", "validate_unit_image", "validate_field", "clamp01",
+           "is_device_array", "to_device", "to_host"]
 
 
 def is_device_array(x) -> bool:
@@ -41,6 +41,37 @@ def validate_image(image):
     if not _finite(arr):
         raise ValueError("image contains non-finite values")
     return arr
+
+
+def validate_unit_image(image):
+    """validate_image followed by the [0, 1] range check (scattering.py:41-45).
+    Returns (image, range_check): the finiteness error is raised here, the
+    range error by range_check() so callers keep the reference's check order.
+    Device tensors need ONE host read for both (finite, min, max)."""
+    if not is_device_array(image):
+        arr = validate_image(image)
+
+        def check():
+            if float(arr.min()) < 0.0 or float(arr.max()) > 1.0:
+                raise ValueError("image values must lie in [0, 1]")
+        return arr, check
+    import torch
+
+    shape = tuple(image.shape)
+    if len(shape) != 3 or shape[2] not in (1, 3):
+        raise ValueError(f"expected (H, W, C) image with C in {{1, 3}}, got shape {shape}")
+    if shape[0] < 1 or shape[1] < 1:
+        raise ValueError(f"image dimensions must be >= 1, got shape {shape}")
+    lo, hi = torch.aminmax(image)
+    stats = torch.stack((torch.isfinite(image).all().to(torch.float64), lo.to(torch.float64),
+                         hi.to(torch.float64))).to("cpu").tolist()
+    if stats[0] != 1.0:
+        raise ValueError("image contains non-finite values")
+
+    def check():
+        if stats[1] < 0.0 or stats[2] > 1.0:
+            raise ValueError("image values must lie in [0, 1]")
+    return image, check
 
 
 def validate_field(field):
@@ -87,7 +118,17 @@ def to_device(x, dtype=None):
 
 
 def to_host(t, like) -> object:
-    """Return `t` as the caller's kind: numpy float64 for host callers."""
+    """Return `t` as the caller's kind: numpy float64 for numpy (host)
+    callers, like the reference; a tensor on the caller's device for torch
+    callers (CPU tensors get the device -> host copy, CUDA tensors none)."""
     if is_device_array(like):
-        return t
+        if like.is_cuda:
+            return t
+        import torch
+
+        # page-locked result (torch's caching host allocator): full-speed copy
+        out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return out
     return t.detach().to("cpu").numpy().astype(np.float64, copy=False)

@@ -29,6 +29,7 @@ from . import _native as nat
 from .config import (ABLATIONS, LAMBDA_MODES, DehazeResult, SolverConfig, SolverTrace,
                      normalize_ablation)
 from .image import (clamp01, is_device_array, to_device, to_host, validate_field,
+                    validate_unit_image,
                     validate_image)
 from .refine import refine_dev
 from .scattering import _airlight_dev, _blend_weights, _dark_dev, _device_vec, _unit_range
@@ -273,12 +274,22 @@ def solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=
     step = cfg.tau if tau is None else float(tau)
     bounds = problem.bounds if problem.bounds is not None else _tau_bounds(problem, cfg,
                                                                           cfg.epsilon)
-    if warn:
-        for b in bounds:
-            if step > b:
-                logger.warning(
-                    "relaxation step %.3g exceeds the stability bound %.3g at the "
-                    "initial iterate; convergence is not guaranteed", step, b)
+    host_bounds = [None]
+
+    def check_bounds():  # solver.py:335-339; device bounds are read after the solve
+        if host_bounds[0] is None:
+            hb = bounds.to("cpu").numpy() if hasattr(bounds, "is_cuda") else np.asarray(bounds)
+            host_bounds[0] = hb
+            if warn:
+                for b in hb:
+                    if step > b:
+                        logger.warning(
+                            "relaxation step %.3g exceeds the stability bound %.3g at the "
+                            "initial iterate; convergence is not guaranteed", step, b)
+        return host_bounds[0]
+
+    if not hasattr(bounds, "is_cuda"):
+        check_bounds()
     P = problem.planes
     prm = _params(problem.height, problem.width, P, problem.channels, cfg,
                   edge_preserving=edge_preserving, tau=step)
@@ -293,6 +304,7 @@ def solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=
                                    norms.ctypes.data, iters.ctypes.data, conv.ctypes.data,
                                    failed.ctypes.data, nat.ptr(ws), ws.numel(),
                                    nat.stream_ptr())
+    bounds = check_bounds()
     if rc == nat.PDZ_ENONFINITE:
         first = int(np.flatnonzero(failed)[0])
         raise FloatingPointError(
@@ -345,7 +357,7 @@ def prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, lambda_mode, phi=None, l
     bounds = torch.empty(c, dtype=torch.float64, device=img_dev.device)
     nat.check(lib.pdz_tau_bound_hwc(prm, nat.ptr(phi64), nat.ptr(lam), nat.ptr(bounds),
                                     nat.ptr(ws), ws.numel(), nat.stream_ptr()))
-    return phi, lam, bounds.to("cpu").numpy()
+    return phi, lam, bounds  # device tensor: read after the solve (one sync less)
 
 
 def fixed_point_solve(channel, transmission, airlight_c: float, cfg: SolverConfig, *,
@@ -430,11 +442,12 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
 
     cfg = cfg or SolverConfig()
     flags = normalize_ablation(ablation)
-    # torch inputs (pinned host or device) are moved first and validated on the GPU
-    img = validate_image(to_device(image) if is_device_array(image) else image)
+    # torch inputs (pinned host or device) are moved first and validated on the
+    # GPU with one combined reduction (finite, min, max: one host read)
+    img, unit_check = validate_unit_image(to_device(image) if is_device_array(image) else image)
     if workers < 1:
         raise ValueError("workers must be >= 1")
-    _unit_range(img)
+    unit_check()
     img_dev, is_f64 = _image_dev(img)
     h, w, c = img_dev.shape
     t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
@@ -493,20 +506,19 @@ def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
                                   phi=phi[i * c:(i + 1) * c], lam=lam[i], with_bounds=True)
         fronts.append((t_dev, a_dev))
         bounds.append(b)
-    problem = DeviceProblem(phi, lam, h, w, B * c, c, np.concatenate(bounds))
+    problem = DeviceProblem(phi, lam, h, w, B * c, c, torch.cat(bounds))
     u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
     lib = nat.lib()
     for i in range(B):
         nat.check(lib.pdz_clamp_interleave(nat.ptr(u[i * c:(i + 1) * c]), h, w, c,
                                            nat.ptr(out[i]), 1, nat.stream_ptr()))
-    host = not is_device_array(images if not isinstance(images, (list, tuple)) else images[0])
+    like = images[0] if isinstance(images, (list, tuple)) else images
     results = []
     for i, (t_dev, a_dev) in enumerate(fronts):
-        results.append(DehazeResult(a_dev.cpu().numpy() if host else a_dev,
-                                    t_dev.cpu().numpy() if host else t_dev,
+        results.append(DehazeResult(to_host(a_dev, like), to_host(t_dev, like),
                                     traces[i * c:(i + 1) * c], flags))
-    return (out.cpu().numpy() if host else out), results
+    return to_host(out, like), results
 
 
 def write_trace_csv(traces, path) -> None:
