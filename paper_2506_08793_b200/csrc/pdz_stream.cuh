@@ -63,6 +63,7 @@ constexpr int kComputeThreads = kSCW * 32;
 // the last compute warp, whose threads carry one horizontal-pass item fewer.
 constexpr int kLead = kComputeThreads - 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
+constexpr int kNBuf = 3;                    // iterate buffers (iteration n in buf[n % 3])
 // Column pad of the padded iterates: 32 floats (128 B) each side, so padded
 // rows and every strip's first image column are 128-byte aligned (only the
 // ceil4(R) columns next to the image are ever written or read).
@@ -89,11 +90,10 @@ struct SGeo {
 struct StreamArgs {
   // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2 kPadC], box
   // {PITCH, kSRB + 2R, 1}.
-  CUtensorMap tm[2];
+  CUtensorMap tm[kNBuf];
   CUtensorMap tm_phi;   // Phi [P][H][W], box {64, kSRB, 1}
   CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, kSRB, 1}
-  float* buf0;
-  float* buf1;
+  float* buf[kNBuf];   // iterate n in buf[n % kNBuf] (padded planes)
   const float* phi;
   const float* lam;
   Partials pt;          // ring of kRing slots
@@ -306,7 +306,7 @@ struct RangeIter {
       const int p = b * a.C + c;
       if (STOP && check_stop) {
         const int st = a.st.stop_iter[p];
-        if (st != 0 && st < iter - 1) {
+        if (st != 0 && st <= iter - kNBuf) {  // its answer buf[st % 3] is kept
           L = seg_end;
           wrap(a);
           continue;
@@ -360,10 +360,10 @@ struct FlatIter {
   __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy_iter,
                                       int* s_progress, const int* s_fin, const int* s_anystop) {
     while (!ended && iter <= a.iter_last) {
-      if (STOP && fresh && a.st.stop_iter && iter > 2) {
-        if (busy_iter && iter - 2 >= busy_iter) return kDefer;
+      if (STOP && fresh && a.st.stop_iter && iter > kNBuf) {
+        if (busy_iter && iter - kNBuf >= busy_iter) return kDefer;
         PDZ_P(const long long tg = global_ns();)
-        wait_shared_ge(s_fin, iter - 2);
+        wait_shared_ge(s_fin, iter - kNBuf);
         PDZ_P(grant_ns += global_ns() - tg;)
         // Only once some plane has stopped are the global stop records
         // consulted (no dependent global load on the per-block path before
@@ -372,7 +372,7 @@ struct FlatIter {
         r.check_stop = ld_acquire_cta_shared(s_anystop) != 0;
         if (r.check_stop) {
           const int all = ld_relaxed(a.flags);
-          if (all != 0 && all <= iter - 2) {
+          if (all != 0 && all <= iter - kNBuf) {
             ended = true;
             break;
           }
@@ -422,7 +422,7 @@ template <int R>
 __device__ __forceinline__ void issue_block(const StreamArgs& a, const LoadReq& q, float* in,
                                             uint64_t* bar) {
   using Gm = SGeo<R>;
-  const int buf = (q.iter - 1) & 1;  // the buffer iteration `iter` reads
+  const int buf = (q.iter - 1) % kNBuf;  // the buffer iteration `iter` reads
   mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
   tma_load_3d(in, &a.tm[buf], q.x0 + kPadC - Gm::RP, q.yb, q.p, bar);
 }
@@ -518,7 +518,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       }
       PDZ_P(const bool ok_dep = __all_sync(0xffffffffu, ok);)
       if (lane == 0 && fin_on) {
-        const int need_fin = STOP ? n - 2 : n - kRing;
+        const int need_fin = STOP ? n - kNBuf : n - kRing;
         if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
       }
       grant = __all_sync(0xffffffffu, ok);
@@ -748,7 +748,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     uint64_t* const bar_cur = &bars[ib];
     const int gx = cur.x0 + c;
     const bool col_ok = gx < W;
-    float* __restrict__ uout_all = (cur.iter & 1) ? a.buf1 : a.buf0;
+    float* __restrict__ uout_all = a.buf[cur.iter % kNBuf];
 
     // (the previous block ended with a CTA barrier: IN(b-1), H and the
     // Phi / lambda tiles are free)

@@ -469,8 +469,8 @@ struct Sync {
 // TMA tensor maps of the two padded iterate buffers for the streaming kernel:
 // a 3-D tensor [P][H + 2R][W + 2 kPadC] float32, box {64 + 2RP + 4, kSRB + 2R, 1};
 // out-of-bounds elements (over-fetch past the last row) zero-fill.
-static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, float* buf0,
-                                  float* buf1, const float* phi, const float* lam,
+static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
+                                  float* const* bufs, const float* phi, const float* lam,
                                   StreamArgs* b) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
@@ -491,8 +491,7 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, flo
   const cuuint64_t dims[3] = {wp, hp, cuuint64_t(p->planes)};
   const cuuint64_t strides[2] = {wp * 4, wp * hp * 4};
   const cuuint32_t estr[3] = {1, 1, 1};
-  float* bufs[2] = {buf0, buf1};
-  for (int bi = 0; bi < 2; ++bi) {
+  for (int bi = 0; bi < kNBuf; ++bi) {
     const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + kSRB), 1};
     CUresult r = encode(&b->tm[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -525,6 +524,7 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl, flo
 }
 
 static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0, float* buf1,
+                         float* buf2,
                          const float* phi, const float* lam, double* psum, int32_t* pflag,
                          const StateView& st, const Sync& sy, LaunchArgs* la) {
   memset(la, 0, sizeof(*la));
@@ -576,8 +576,9 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   a.row_hi = p->height;
   memcpy(a.w, w, sizeof(w));
   StreamArgs& b = la->stream;
-  b.buf0 = buf0;
-  b.buf1 = buf1;
+  b.buf[0] = buf0;
+  b.buf[1] = buf1;
+  b.buf[2] = buf2;
   b.phi = phi;
   b.lam = lam;
   b.pt = pt;
@@ -608,7 +609,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.rel_tol = p->rel_tol;
   memcpy(b.w, w, sizeof(w));
   for (int i = 0; i < kMaxTaps; ++i) b.w2[i] = make_float2(w[i], w[i]);
-  if (pl.stream) return encode_stream_maps(p, pl, buf0, buf1, phi, lam, &b);
+  if (pl.stream) return encode_stream_maps(p, pl, b.buf, phi, lam, &b);
   return PDZ_OK;
 }
 
@@ -676,6 +677,7 @@ __global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict
 // Dense final iterate: plane p from buf[iters[p] & 1] (the last iteration whose
 // norm was recorded; solver.py:359), interior of the padded layout.
 __global__ void extract_kernel(const float* __restrict__ buf0, const float* __restrict__ buf1,
+                               const float* __restrict__ buf2, int nbuf,
                                const int32_t* __restrict__ iters, float* __restrict__ out, int H,
                                int W, int P, int pr, int pc) {
   const int wp = W + 2 * pc, hp = H + 2 * pr;
@@ -684,14 +686,16 @@ __global__ void extract_kernel(const float* __restrict__ buf0, const float* __re
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pl = i / (int64_t(H) * W);
     const int y = int((i / W) % H), x = int(i % W);
-    const float* src = (iters[pl] & 1) ? buf1 : buf0;
+    const int k = iters[pl] % nbuf;
+    const float* src = k == 0 ? buf0 : (k == 1 ? buf1 : buf2);
     out[i] = src[(pl * hp + y + pr) * wp + x + pc];
   }
 }
 
 struct SolveLayout {
-  float* buf0;  // iterate ping-pong buffers (padded for the streaming kernel)
+  float* buf0;  // iterate buffers: tiled ping-pong / persistent triple (padded)
   float* buf1;
+  float* buf2;  // persistent kernel only
   float* out;   // dense final iterate [P][H][W] (pdz_fixed_point_sweeps_async)
   double* psum;
   int32_t* pflag;
@@ -709,6 +713,7 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   L.out = c.take<float>(P * plane);  // first: same offset under either plan
   L.buf0 = c.take<float>(P * plane_pad);
   L.buf1 = c.take<float>(P * plane_pad);
+  L.buf2 = pl.stream ? c.take<float>(P * plane_pad) : nullptr;
   L.psum = c.take<double>(size_t(pl.ring) * P * pl.nbmax);
   L.pflag = c.take<int32_t>(size_t(pl.ring) * P * pl.nbmax);
   L.st.stop_iter = c.take<int32_t>(P);
@@ -800,7 +805,8 @@ static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const So
                              float* out, cudaStream_t s) {
   const int64_t n = int64_t(p->planes) * p->height * p->width;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
-  extract_kernel<<<blocks, 256, 0, s>>>(L.buf0, L.buf1, L.st.iters, out, p->height, p->width,
+  extract_kernel<<<blocks, 256, 0, s>>>(L.buf0, L.buf1, L.buf2, pl.stream ? kNBuf : 2,
+                                        L.st.iters, out, p->height, p->width,
                                         p->planes, pl.pad_r, pl.pad_c);
   PDZ_CHECK_LAUNCH("extract");
   return PDZ_OK;
@@ -810,7 +816,8 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
                            const float* phi, const float* lam, float* out, cudaStream_t s,
                            bool poll) {
   LaunchArgs la;
-  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, phi, lam, L.psum, L.pflag, L.st, L.sy, &la);
+  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, L.buf2, phi, lam, L.psum, L.pflag, L.st, L.sy,
+                         &la);
   if (rc != PDZ_OK) return rc;
   {
     const int64_t n = int64_t(p->planes) * (p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
@@ -939,8 +946,8 @@ static int32_t step_impl(const pdz_solve_params* params, const float* u, float* 
   LaunchArgs la;
   StateView none = {};
   // iteration 1 reads buf0 (= u), writes buf1 (= u_out)
-  rc = fill_args(&one, pl, const_cast<float*>(u), u_out, phi, lambda_map, psum, pflag, none, sy,
-                 &la);
+  rc = fill_args(&one, pl, const_cast<float*>(u), u_out, nullptr, phi, lambda_map, psum, pflag,
+                 none, sy, &la);
   if (rc != PDZ_OK) return rc;
   la.tile.y_off = y_off;
   la.tile.H_glob = H_glob;
