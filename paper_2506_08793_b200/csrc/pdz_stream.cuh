@@ -109,6 +109,7 @@ struct StreamArgs {
   long long* prof;      // -DPDZ_PROFILE builds + PDZ_PROF=1: [2G+1][16] wait times
   float w[kMaxTaps];
   float2 w2[kMaxTaps];  // (w, w) pairs: the FFMA2 operand
+  float2 wp[kMaxTaps + 1];  // (w[k], w[k-1]), w[-1] = w[K] = 0: horizontal-pass output pairs
 };
 
 // Profiling instrumentation (tools/prof_stream.py): compiled only with
@@ -792,15 +793,22 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
       }
-      // packed FFMA2 over output pairs (per-lane fma.rn, same order as scalar)
+      // packed FFMA2 over output pairs (2m, 2m+1): staged value j, broadcast
+      // to both lanes (FFMA2 .F32 operand, no register-pair shuffles), meets
+      // taps (w[j-2m], w[j-2m-1]).  Per lane the terms arrive in tap order,
+      // plus one exact +0*v at the unused end, so each output is bitwise the
+      // scalar fma chain.
       float2 o[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) o[m] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k <= 2 * R; ++k) {
+      for (int j = 0; j < 2 * R + 8; ++j) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
-          o[m] = ffma2(a.w2[k], make_float2(v[OFF + k + 2 * m], v[OFF + k + 2 * m + 1]), o[m]);
+        for (int m = 0; m < 4; ++m) {
+          const int t = j - 2 * m;
+          if (t >= 0 && t <= 2 * R + 1)
+            o[m] = ffma2(make_float2(v[OFF + j], v[OFF + j]), a.wp[t], o[m]);
+        }
       }
       float4* dst = reinterpret_cast<float4*>(h_cur + i * Gm::HP + 8 * g);
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
@@ -830,18 +838,21 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       // rolling window of u rows (A = y-1, B = y, C = y+1) at columns c-1 .. c+2
       // (staged column RP + c is 8-byte aligned)
       const float* urow = in_cur + (R + j0 - 1) * Gm::PITCH + Gm::RP + c;
-      const float sx0 = (gx == 0) ? 1.0f : 0.5f;          // column c   (c >= 0)
-      const float sx1 = (gx + 1 == W - 1) ? 1.0f : 0.5f;  // column c+1
-      const float2 half2 = make_float2(0.5f, 0.5f), eps2 = make_float2(a.eps, a.eps);
+      // np.gradient factors (1 at the one-sided ends, else 1/2) times the 1/2
+      // of the face average, applied once to the summed raw differences:
+      // both are powers of two, so this is bitwise the factored form
+      const float2 hx2 = make_float2((gx == 0) ? 0.5f : 0.25f,            // column c
+                                     (gx + 1 == W - 1) ? 0.5f : 0.25f);  // column c+1
+      const float2 eps2 = make_float2(a.eps, a.eps);
       float2 eA = make_float2(urow[-1], urow[2]);
       float2 cA = *reinterpret_cast<const float2*>(urow);
       urow += Gm::PITCH;
       float2 eB = make_float2(urow[-1], urow[2]);
       float2 cB = *reinterpret_cast<const float2*>(urow);
-      float2 xA = make_float2(sx0 * (cA.y - eA.x), sx1 * (eA.y - cA.x));
-      float2 xB = make_float2(sx0 * (cB.y - eB.x), sx1 * (eB.y - cB.x));
+      float2 xA = make_float2(cA.y - eA.x, eA.y - cA.x);  // raw centred x-differences
+      float2 xB = make_float2(cB.y - eB.x, eB.y - cB.x);
       // south flux of the row above the first output row
-      float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(half2, add2(xA, xB)), eps2);
+      float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(hx2, add2(xA, xB)), eps2);
       float2 r2p = make_float2(0.f, 0.f), nfp = make_float2(0.f, 0.f);
       const float2 zero2 = make_float2(0.f, 0.f), tau2 = make_float2(a.tau, a.tau);
       float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + kPadC;
@@ -869,19 +880,20 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
           urow += Gm::PITCH;
           const float2 eC = make_float2(urow[-1], urow[2]);
           const float2 cC = *reinterpret_cast<const float2*>(urow);
-          const float2 xC = make_float2(sx0 * (cC.y - eC.x), sx1 * (eC.y - cC.x));
-          const float sy = (j == jz0 || j == jz1) ? 1.0f : 0.5f;
-          const float2 sy2 = make_float2(sy, sy);
-          // centred vertical differences: d = columns (c, c+1), de = (c-1, c+2)
-          const float2 d = mul2(sy2, sub2(cC, cA));
-          const float2 de = mul2(sy2, sub2(eC, eA));
+          const float2 xC = make_float2(cC.y - eC.x, eC.y - cC.x);
+          // rows 0 / H-1 (one-sided) only occur in warps that also mirror
+          const float hy = (MIR && (j == jz0 || j == jz1)) ? 0.5f : 0.25f;
+          const float2 hy2 = make_float2(hy, hy);
+          // raw centred vertical differences: d = columns (c, c+1), de = (c-1, c+2)
+          const float2 d = sub2(cC, cA);
+          const float2 de = sub2(eC, eA);
           const float u0 = cB.x, u1 = cB.y;
           // east faces c-1|c and c+1|c+2 as one pair: the second with its jump
           // negated, (u0 - l, u1 - r) = cB - eB; sflux is odd in the jump, so
           // the pair is (fw, -fe) exactly
-          const float2 fwe = sflux2<EDGE>(sub2(cB, eB), mul2(half2, add2(de, d)), eps2);
-          const float fm = sflux<EDGE>(u1 - u0, 0.5f * (d.x + d.y), a.eps);  // face c|c+1
-          const float2 fs_dn = sflux2<EDGE>(sub2(cC, cB), mul2(half2, add2(xB, xC)), eps2);
+          const float2 fwe = sflux2<EDGE>(sub2(cB, eB), mul2(hy2, add2(de, d)), eps2);
+          const float fm = sflux<EDGE>(u1 - u0, hy * (d.x + d.y), a.eps);  // face c|c+1
+          const float2 fs_dn = sflux2<EDGE>(sub2(cC, cB), mul2(hx2, add2(xB, xC)), eps2);
           // div0 = ((fm - fw) + s0) - n0, div1 = ((fe - fm) + s1) - n1, with
           // fe - fm = -(fm + (-fe)) exactly
           const float2 div = sub2(add2(make_float2(fm - fwe.x, -(fm + fwe.y)), fs_dn), fs_up);

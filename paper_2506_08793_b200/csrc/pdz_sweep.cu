@@ -609,6 +609,8 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.rel_tol = p->rel_tol;
   memcpy(b.w, w, sizeof(w));
   for (int i = 0; i < kMaxTaps; ++i) b.w2[i] = make_float2(w[i], w[i]);
+  for (int i = 0; i <= kMaxTaps; ++i)
+    b.wp[i] = make_float2(i < kMaxTaps ? w[i] : 0.f, i > 0 ? w[i - 1] : 0.f);
   if (pl.stream) return encode_stream_maps(p, pl, b.buf, phi, lam, &b);
   return PDZ_OK;
 }
