@@ -17,11 +17,13 @@
 //    C - 1 passes earlier, so in steady state nobody waits.  A per-CTA
 //    progress counter (passes completed) carries that ordering (release /
 //    acquire); the same wait protects the ping-pong buffer being overwritten.
-//  * the two iterate buffers are PADDED, [P][H + 2R][W + 2 ceil4(R)]: the
-//    producer of an output near an image border also stores its mirrored
-//    copies into the pads (np.pad "symmetric", solver.py:235), so no reader
-//    ever reflects an index.  Each block's input rows (64 + 2 ceil4(R)
-//    columns) arrive by ONE TMA tile load (cp.async.bulk.tensor, UTMALDG)
+//  * the iterate buffers are PADDED, [P][H + 2R][W + 2 kPadC], so every
+//    block's staged box is a plain box of the padded tensor; a block that
+//    touches an image border reflects its staged pads in shared memory from
+//    the interior values of the same tile (np.pad "symmetric",
+//    solver.py:235) -- nothing mirrored is stored globally.  Each block's
+//    input rows (64 + 2 ceil4(R) columns) arrive by ONE TMA tile load
+//    (cp.async.bulk.tensor, UTMALDG)
 //    into a double buffer, signalled by an mbarrier and always queued one
 //    block ahead -- across pass boundaries too.
 //  * horizontal Gaussian from shared memory (8 outputs per item), vertical
@@ -330,7 +332,6 @@ struct RangeIter {
 __device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter - 1) * C + c + 1; }
 
 enum { kEnd = 0, kBlock = 1, kDefer = 2 };
-constexpr int kNoMirror = -0x40000000;
 
 // Spin on a shared-memory value written by the service warp; a wait that
 // outlives the spin timeout traps (the service warp has already flagged the
@@ -770,18 +771,39 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       PDZ_PT(3, mbar_wait(bar_cur, phase0));
       phase0 ^= 1;
     }
-    PDZ_P(pf[11] += global_ns() - tph; tph = global_ns();)
+    PDZ_P(pf[11] += global_ns() - tph; tph = global_ns(); pf[14] += tph - tn_; const long long tdata = tph;)
+    const int hn = cur.n + 2 * R;
+    // ---- image borders (np.pad "symmetric", solver.py:235: -1-i <- i,
+    // H+i <- H-1-i): nothing mirrored is stored globally and the pads of the
+    // global iterates never carry data.  The horizontal pass reads a pad
+    // row's mirror source row and patches pad columns in registers; the
+    // vertical pass patches its border loads.  Only a partial last strip
+    // (W % 64 != 0) reflects its right pad columns in shared memory first.
+    const int ylo = cur.yb - R;  // image row of staged row 0
+    const bool lbord = cur.x0 == 0;
+    const int wl = W - cur.x0;   // image columns of the strip
+    const bool rbord = wl == kSTW;
+    if (wl < kSTW) {  // CTA-uniform
+      const int xr = Gm::RP + wl;  // staged column of image column W
+      const int k = tid & 15;
+      static_assert(Gm::RP <= 16, "pad columns per row slot");
+      if (k < Gm::RP && xr + k < Gm::PWD)
+        for (int sr = tid >> 4; sr < hn; sr += kComputeThreads / 16)
+          in_cur[sr * Gm::PITCH + xr + k] = in_cur[sr * Gm::PITCH + xr - 1 - k];
+      compute_bar();
+    }
     // ---- H rows: horizontal blur of the n + 2R staged rows
     // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R)
     // staged values per 8 outputs.
     // Item -> (row i, column group g): 8 consecutive items = 8 consecutive rows
     // of one group (a conflict-free quarter-warp, see SGeo).
-    const int hn = cur.n + 2 * R;
     const int hitems = ((hn + 7) & ~7) * (kSTW / 8);
     for (int item = tid; item < hitems; item += kComputeThreads) {
       const int i = (item >> 6) * 8 + (item & 7), g = (item >> 3) & 7;
       if (i >= hn) continue;
-      const float* row = in_cur + i * Gm::PITCH + 8 * g;
+      const int y = ylo + i;  // a pad row reads its mirror source row
+      const int si = (y < 0 ? -1 - y : (y >= H ? 2 * H - 1 - y : y)) - ylo;
+      const float* row = in_cur + si * Gm::PITCH + 8 * g;
       constexpr int OFF = Gm::RP - R;
       constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
       float v[4 * NQ];
@@ -792,6 +814,29 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         v[4 * q + 1] = t.y;
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
+      }
+      // pad columns in registers: left (staged column t < RP of group 0)
+      // <- 2 RP - 1 - t; right (full last strip, staged column 8g + t >= RP +
+      // 64) <- 2 RP + 127 - 8g - t.  Compile-time indices per group.
+      if (lbord && g == 0) {
+#pragma unroll
+        for (int t = OFF; t < Gm::RP; ++t) v[t] = v[2 * Gm::RP - 1 - t];
+      }
+      if (rbord && g >= 5) {
+        auto patch = [&](auto gtag) {
+          constexpr int GG = decltype(gtag)::value;
+#pragma unroll
+          for (int t = OFF; t < OFF + 2 * R + 8; ++t) {
+            const int tp = 2 * Gm::RP + 127 - 16 * GG - t;
+            if (8 * GG + t >= Gm::RP + kSTW && tp >= 0 && tp < 4 * NQ) v[t] = v[tp];
+          }
+        };
+        if (g == 7)
+          patch(std::integral_constant<int, 7>{});
+        else if (g == 6)
+          patch(std::integral_constant<int, 6>{});
+        else
+          patch(std::integral_constant<int, 5>{});
       }
       // packed FFMA2 over output pairs (2m, 2m+1): staged value j, broadcast
       // to both lanes (FFMA2 .F32 operand, no register-pair shuffles), meets
@@ -844,45 +889,56 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       const float2 hx2 = make_float2((gx == 0) ? 0.5f : 0.25f,            // column c
                                      (gx + 1 == W - 1) ? 0.5f : 0.25f);  // column c+1
       const float2 eps2 = make_float2(a.eps, a.eps);
-      float2 eA = make_float2(urow[-1], urow[2]);
-      float2 cA = *reinterpret_cast<const float2*>(urow);
-      urow += Gm::PITCH;
-      float2 eB = make_float2(urow[-1], urow[2]);
-      float2 cB = *reinterpret_cast<const float2*>(urow);
-      float2 xA = make_float2(cA.y - eA.x, eA.y - cA.x);  // raw centred x-differences
-      float2 xB = make_float2(cB.y - eB.x, eB.y - cB.x);
-      // south flux of the row above the first output row
-      float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(hx2, add2(xA, xB)), eps2);
       float2 r2p = make_float2(0.f, 0.f), nfp = make_float2(0.f, 0.f);
       const float2 zero2 = make_float2(0.f, 0.f), tau2 = make_float2(a.tau, a.tau);
       float* __restrict__ uout = uout_all + cur.p * plane_pad + size_t(R) * WP + kPadC;
-      // mirrored copies for the pads (np.pad "symmetric": -1-i <- i, W+i <- W-1-i):
-      // the reversed column pair at column xm; rows j < jt also go to row
-      // -1-y, rows j >= jb to row 2H-1-y.  Warps without a border thread run
-      // the loop without any mirror code (warp-uniform choice).
-      const int xm = gx < RP ? -2 - gx : (gx >= W - RP ? 2 * W - 2 - gx : kNoMirror);
       const int y0 = cur.yb + j0;  // image row of j = 0
-      const int jt = R - y0, jb = H - R - y0;
-      const bool mir = jt > 0 || jb < kRPW || xm != kNoMirror;
       const int jz0 = -y0, jz1 = H - 1 - y0;  // rows 0 / H-1: one-sided differences
+      // warps holding row 0 or H-1 run the loop with the per-row factor test
+      // and the row-pad patches; warps of a border strip patch the pad
+      // columns of their loads (u[-1] = u[0], u[W] = u[W-1])
+      const bool edge_row = (jz0 >= 0 && jz0 < kRPW) || (jz1 >= 0 && jz1 < kRPW);
+      const bool edge_col = lbord || wl <= kSTW;
+      const bool pcl = gx == 0, pcr = gx + 1 == W - 1;
       const int nrows = col_ok ? min(kRPW, cur.n - j0) : 0;
       float* orow = uout + ptrdiff_t(y0) * WP + gx;
       const float* pl_row = sphi + j0 * kSTW + c;  // Phi / lambda tiles: row pitch 64
       const float* lm_row = slam + j0 * kSTW + c;
-      auto rows = [&](auto mirror_tag) {
-        constexpr bool MIR = decltype(mirror_tag)::value;
-        const int dx = xm != kNoMirror ? xm - gx : 0;  // column offset of the mirror pair
-        float* const top = uout + ptrdiff_t(-1 - y0) * WP + gx;  // row -1-y at j = 0
-        float* const bot = uout + ptrdiff_t(2 * H - 1 - y0) * WP + gx;  // row 2H-1-y
+      auto rows = [&](auto erow_tag, auto ecol_tag) {
+        constexpr bool EROW = decltype(erow_tag)::value;
+        constexpr bool ECOL = decltype(ecol_tag)::value;
+        // Column pairs in packed float2: c = (u[c], u[c+1]), e = (u[c-1], u[c+2]).
+        auto load = [&](float2& e, float2& cc) {
+          e = make_float2(urow[-1], urow[2]);
+          cc = *reinterpret_cast<const float2*>(urow);
+          if (ECOL) {
+            if (pcl) e.x = cc.x;
+            if (pcr) e.y = cc.y;
+          }
+        };
+        float2 eA, cA, eB, cB;
+        load(eA, cA);
+        urow += Gm::PITCH;
+        load(eB, cB);
+        if (EROW && jz0 == 0) {  // row -1 = row 0
+          eA = eB;
+          cA = cB;
+        }
+        float2 xA = make_float2(cA.y - eA.x, eA.y - cA.x);  // raw centred x-differences
+        float2 xB = make_float2(cB.y - eB.x, eB.y - cB.x);
+        // south flux of the row above the first output row
+        float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(hx2, add2(xA, xB)), eps2);
 #pragma unroll
         for (int j = 0; j < kRPW; ++j) {
-          // Column pairs in packed float2: c = (u[c], u[c+1]), e = (u[c-1], u[c+2]).
           urow += Gm::PITCH;
-          const float2 eC = make_float2(urow[-1], urow[2]);
-          const float2 cC = *reinterpret_cast<const float2*>(urow);
+          float2 eC, cC;
+          load(eC, cC);
+          if (EROW && j == jz1) {  // row H = row H-1
+            eC = eB;
+            cC = cB;
+          }
           const float2 xC = make_float2(cC.y - eC.x, eC.y - cC.x);
-          // rows 0 / H-1 (one-sided) only occur in warps that also mirror
-          const float hy = (MIR && (j == jz0 || j == jz1)) ? 0.5f : 0.25f;
+          const float hy = (EROW && (j == jz0 || j == jz1)) ? 0.5f : 0.25f;
           const float2 hy2 = make_float2(hy, hy);
           // raw centred vertical differences: d = columns (c, c+1), de = (c-1, c+2)
           const float2 d = sub2(cC, cA);
@@ -912,27 +968,22 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
           const float r0 = rr.x, r1 = rr.y, n0 = nn.x, n1 = nn.y;
           if (j < nrows) {
             *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
-            if (MIR) {
-#ifndef PDZ_NO_MIRROR_STORES  // (profiling experiment only)
-              const bool ym = j < jt || j >= jb;
-              float* const mrow = (j < jt ? top : bot) - ptrdiff_t(j) * WP;
-              if (ym) *reinterpret_cast<float2*>(mrow) = make_float2(n0, n1);
-              if (dx != 0) {
-                *reinterpret_cast<float2*>(orow + dx) = make_float2(n1, n0);
-                if (ym) *reinterpret_cast<float2*>(mrow + dx) = make_float2(n1, n0);
-              }
-#endif
-            }
             r2p = ffma2(rr, rr, r2p);
             nfp = ffma2(nn, zero2, nfp);  // NaN iff non-finite update
           }
           orow += WP;
         }
       };
-      if (__any_sync(0xffffffffu, mir))
-        rows(std::true_type{});
-      else
-        rows(std::false_type{});
+      if (edge_row) {  // warp-uniform (the warp's rows) / CTA-uniform (the strip)
+        if (edge_col)
+          rows(std::true_type{}, std::true_type{});
+        else
+          rows(std::true_type{}, std::false_type{});
+      } else if (edge_col) {
+        rows(std::false_type{}, std::true_type{});
+      } else {
+        rows(std::false_type{}, std::false_type{});
+      }
       acc_r2 += double(r2p.x + r2p.y);
       acc_nf += nfp.x + nfp.y;
     }
@@ -953,6 +1004,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     // store of the block precede this barrier (it also orders the pass's
     // outputs before the progress flag)
     PDZ_PT(5, compute_bar());
+    PDZ_P(pf[13] += global_ns() - tdata;)
     if (flush) {
       if (tid == kLead) {
         double t = 0.0;

@@ -336,7 +336,11 @@ def test_batch_equals_single(pdz):
 
 @pytest.mark.parametrize("shape,k", [((2, 2), 5), ((2, 9), 13), ((5, 3), 49), ((33, 65), 19),
                                      ((64, 32), 25), ((67, 95), 3), ((130, 70), 1),
-                                     ((70, 40), 15), ((40, 70), 97)])
+                                     ((70, 40), 15), ((40, 70), 97),
+                                     # streaming kernel: partial last strip (W % 64 != 0),
+                                     # full border strips at every compiled radius
+                                     ((96, 100), 19), ((50, 68), 25), ((80, 132), 13),
+                                     ((72, 128), 25), ((40, 192), 5), ((36, 64), 7)])
 def test_odd_shapes_against_oracle(pdz, shape, k):
     rng = np.random.default_rng(sum(shape) + k)
     ch = rng.random(shape) * 0.8 + 0.1

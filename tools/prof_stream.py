@@ -42,7 +42,9 @@ G = int(((buf[:4096, 6] > 0) & (buf[:4096, 12] > 0)).sum())
 g = buf[:G]
 sv = buf[G + 1:2 * G + 1]
 names = ["total", "grant", "topbar", "mbar", "hbar", "flushbar", "blocks", "defers",
-         "mirror", "hpass", "vpass", "prefetch", "next"]
+         "mirror", "hpass", "vpass", "prefetch", "next", "compute", "towait"]
+os.makedirs("gpurun_out", exist_ok=True)
+np.save("gpurun_out/prof_raw.npy", buf[:2 * G + 1])
 print(f"G={len(g)}  iters={iters}  per-sweep us (mean / min / max over CTAs):")
 for i, n in enumerate(names):
     v = g[:, i] / iters if i in (6, 7) else g[:, i] / (1e3 * iters)
@@ -78,3 +80,10 @@ for i in np.argsort(-g[:, 10])[:16]:
           f"vpass={g[i, 10] / 1e3 / iters:6.2f} hpass={g[i, 9] / 1e3 / iters:6.2f} "
           f"mbar={g[i, 3] / 1e3 / iters:6.2f}")
 print("fastest by vpass:", ", ".join(f"{i}:{g[i, 10] / 1e3 / iters:.2f}" for i in np.argsort(g[:, 10])[:6]))
+
+print("per-CTA compute (data ready -> end barrier) and lead-warp wait (loop top -> data), us/sweep:")
+comp = g[:, 13] / 1e3 / iters
+wt = g[:, 14] / 1e3 / iters
+for i in np.argsort(-comp)[:20]:
+    print(f"  cta {i:4d} compute {comp[i]:6.2f}  wait {wt[i]:6.2f}  hpass {g[i, 9] / 1e3 / iters:5.2f} vpass {g[i, 10] / 1e3 / iters:5.2f}")
+print("compute: mean %.2f min %.2f max %.2f" % (comp.mean(), comp.min(), comp.max()))
