@@ -777,13 +777,14 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     // H+i <- H-1-i): nothing mirrored is stored globally and the pads of the
     // global iterates never carry data.  The horizontal pass reads a pad
     // row's mirror source row and patches pad columns in registers; the
-    // vertical pass patches its border loads.  Only a partial last strip
-    // (W % 64 != 0) reflects its right pad columns in shared memory first.
+    // vertical pass patches its border loads.  When W % 64 != 0 the strips
+    // whose staged columns reach past W (the last one or two) reflect their
+    // right pad columns in shared memory first.
     const int ylo = cur.yb - R;  // image row of staged row 0
     const bool lbord = cur.x0 == 0;
     const int wl = W - cur.x0;   // image columns of the strip
     const bool rbord = wl == kSTW;
-    if (wl < kSTW) {  // CTA-uniform
+    if (wl != kSTW && wl < kSTW + Gm::RP) {  // CTA-uniform
       const int xr = Gm::RP + wl;  // staged column of image column W
       const int k = tid & 15;
       static_assert(Gm::RP <= 16, "pad columns per row slot");
