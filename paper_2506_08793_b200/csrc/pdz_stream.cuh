@@ -60,10 +60,6 @@ constexpr int kRPW = 6;                     // output rows per compute warp
 constexpr int kSRB = kSCW * kRPW;           // output rows per block
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
-// The compute thread that does the CTA's serial bookkeeping (posting loads,
-// the Phi / lambda TMA, the partial sums, the progress counter): lane 0 of
-// the last compute warp, whose threads carry one horizontal-pass item fewer.
-constexpr int kLead = kComputeThreads - 32;
 constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
 constexpr int kNBuf = 3;                    // iterate buffers (iteration n in buf[n % 3])
 // Column pad of the padded iterates: 32 floats (128 B) each side, so padded
@@ -269,8 +265,8 @@ __device__ __forceinline__ float2 sflux2(float2 jump, float2 along, float2 eps2)
 
 // ----------------------------------------------------------- iteration --
 struct SBlock {
-  int p, x0, yb, n;         // plane, strip origin, first row, rows
-  int iter, c, pass_start;  // pass (iter, c); first block of the pass
+  int p, x0, yb, n;  // plane, strip origin, first row, rows
+  int iter, c;       // pass (iter, c)
 };
 
 // One pass over the CTA's range [L0, L1) of strip-rows: (image b, strip s,
@@ -331,48 +327,26 @@ struct RangeIter {
 // Progress counter value once pass (n, c) is complete.
 __device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter - 1) * C + c + 1; }
 
-enum { kEnd = 0, kBlock = 1, kDefer = 2 };
-
-// Spin on a shared-memory value written by the service warp; a wait that
-// outlives the spin timeout traps (the service warp has already flagged the
-// abort) instead of hanging the GPU.
-__device__ __forceinline__ void wait_shared_ge(const int* p, int v) {
-  if (ld_acquire_cta_shared(p) >= v) return;
-  const long long t0 = global_ns();
-  while (ld_acquire_cta_shared(p) < v) {
-    if (global_ns() - t0 > 2 * kSpinTimeoutNs) __trap();
-    __nanosleep(32);
-  }
-}
-
-// Flat stream of (iteration, channel, block).  Passes with no blocks (every
-// plane of the range frozen) are skipped.  With the stop rule a pass of
-// iteration n first needs the stop decisions of n - 2 (s_fin, mirrored by the
-// service warp); `busy_iter` = iteration of a block still in flight (0: none)
-// -- a pass whose decisions need that block's own completion is deferred
-// (kDefer) until the CTA is idle, so a CTA never waits on itself.  When idle,
-// skipped passes are published at once.
-struct FlatIter {
+// Flat stream of (iteration, channel, block) run by the service warp.
+// Passes with no blocks (every plane of the range frozen) are skipped.  With
+// the stop rule a pass of iteration n first needs the stop decisions of
+// n - 3 (fin >= n - 3: its answer buffer is then final); next() returns
+// kWaitFin until they are known.
+enum { kIterEnd = 0, kIterBlock = 1, kIterWaitFin = 2 };
+struct SvcIter {
   RangeIter r;
   int iter, c;
-  bool fresh;  // next block starts a new pass
+  bool fresh;  // the next block starts a new pass
   bool ended;
-  PDZ_P(long long grant_ns;)
   template <bool STOP>
-  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int busy_iter,
-                                      int* s_progress, const int* s_fin, const int* s_anystop) {
+  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int fin_seen,
+                                      bool anystop) {
     while (!ended && iter <= a.iter_last) {
       if (STOP && fresh && a.st.stop_iter && iter > kNBuf) {
-        if (busy_iter && iter - kNBuf >= busy_iter) return kDefer;
-        PDZ_P(const long long tg = global_ns();)
-        wait_shared_ge(s_fin, iter - kNBuf);
-        PDZ_P(grant_ns += global_ns() - tg;)
-        // Only once some plane has stopped are the global stop records
-        // consulted (no dependent global load on the per-block path before
-        // that).  A stop at iteration <= iter - 2 is mirrored before fin
-        // reaches it, so both tests are uniform across threads.
-        r.check_stop = ld_acquire_cta_shared(s_anystop) != 0;
-        if (r.check_stop) {
+        if (fin_seen < iter - kNBuf) return kIterWaitFin;
+        // Only once some plane has stopped are the stop records consulted.
+        r.check_stop = anystop;
+        if (anystop) {
           const int all = ld_relaxed(a.flags);
           if (all != 0 && all <= iter - kNBuf) {
             ended = true;
@@ -383,12 +357,9 @@ struct FlatIter {
       if (r.template next<STOP>(a, iter, c, blk)) {
         blk.iter = iter;
         blk.c = c;
-        blk.pass_start = fresh;
         fresh = false;
-        return kBlock;
+        return kIterBlock;
       }
-      if (!busy_iter && threadIdx.x == kLead)
-        st_release_cta_shared(s_progress, pass_index(iter, c, a.C));
       if (++c == a.C) {
         c = 0;
         ++iter;
@@ -397,7 +368,7 @@ struct FlatIter {
       fresh = true;
     }
     ended = true;
-    return kEnd;
+    return kIterEnd;
   }
   // Progress index of the last pass before the iterator position.
   __device__ __forceinline__ int completed(const StreamArgs& a) const {
@@ -405,23 +376,13 @@ struct FlatIter {
   }
 };
 
-// A TMA request posted by compute thread 0 for the service warp: load block
-// (p, x0, yb) of iteration `iter`'s input into IN buffer `ib` once pass `k`
-// is granted.
-struct LoadReq {
-  int p, x0, yb, iter, ib, k;
-  PDZ_P(long long t_post;)
-};
-
 // ----------------------------------------------------------- row loads --
-// ONE TMA tile load brings a block's input rows.  The iterate buffers are
-// padded ([P][H + 2R][W + 2 kPadC], the pads holding the symmetric reflection
-// written by the producers), so every needed row and column -- image borders
-// included -- is a plain box of the padded tensor.  Staged row i holds image
-// row yb - R + i (padded row yb + i); rows beyond the block's n + 2R are
-// over-fetch, never read.
+// ONE TMA tile load brings a block's input rows: staged row i holds image row
+// yb - R + i (padded row yb + i); rows beyond the block's n + 2R are
+// over-fetch, never read.  Pad rows / columns of the box are reflected by
+// the readers (the pads of the iterates carry no data).
 template <int R>
-__device__ __forceinline__ void issue_block(const StreamArgs& a, const LoadReq& q, float* in,
+__device__ __forceinline__ void issue_block(const StreamArgs& a, const SBlock& q, float* in,
                                             uint64_t* bar) {
   using Gm = SGeo<R>;
   const int buf = (q.iter - 1) % kNBuf;  // the buffer iteration `iter` reads
@@ -466,110 +427,195 @@ __device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Shared-memory mailbox between the compute warps and the service warp.
+// Non-blocking mbarrier phase test (acquire at CTA scope when complete).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Shared-memory mailbox between the service warp and the compute warps.
 struct Mailbox {
-  int progress;  // passes completed (compute thread 0, after a CTA barrier)
-  int exit;      // compute warps are done
-  int fin;       // mirror of the global `fin` (service warp)
-  int req_seq;   // TMA requests posted (compute thread 0)
-  LoadReq req[2];  // request s in req[s & 1]: at most two outstanding (IN(b), IN(b+1))
-  int anystop;   // some plane has stopped (service warp; released before `fin`)
+  SBlock desc[2];        // block of IN buffer ib (n == 0: end of the stream)
+  SBlock q[4];           // service warp: generated blocks, ring by block number
+  double red[2][kSCW];   // per-warp r^2 of block b in red[b & 1]
+  int nf[2][kSCW];       // per-warp non-finite flag
 };
 
-// Warp kSCW runs every gpu-scope synchronisation of its CTA, so compute warps
-// never execute a gpu-scope fence (which would wait for their in-flight
-// output stores) and never wait for a neighbour -- only for their data.  One
-// fence per round serves every direction:
-//  * publish: the compute warps' completed-pass counter is released to
-//    done[cta];
-//  * load: the posted TMA request for a block of pass k = (n, c) is issued
-//    once k is granted: the CTAs whose rows it reads have published pass
-//    (n-1, c), partial slot n % kRing is free (fin >= n - kRing) and, with the
-//    stop rule, fin >= n - 2 (once every plane has stopped, anything goes);
-//  * fin: with the stop rule, the global `fin` is mirrored for the iterator.
+// The service warp (warp kSCW) runs the CTA's whole schedule, so the compute
+// warps only wait for data, compute and report:
+//  * it walks the block stream (SvcIter) and posts each block's descriptor
+//    with the TMA load of its input rows into IN(b & 1), once the pass is
+//    granted: the CTAs whose rows the stencil reads have published pass
+//    (n-1, c), partial slot n % kRing is free (fin >= n - kRing), and the
+//    buffer's previous block b-2 is done;
+//  * when the compute warps report block b done (mbarrier bars[3 + (b & 1)],
+//    one arrival per warp), it sums their r^2 in a fixed order into the
+//    (CTA, plane, iteration) partial slot and publishes the CTA's progress
+//    (passes completed) to done[cta];
+//  * with the stop rule it mirrors `fin` for the iterator.
+// Every gpu-scope fence of the CTA is executed here, one per round for all
+// purposes (release of the progress, acquire of neighbours / fin).
 template <int R, bool STOP>
 __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float* in1,
-                             uint64_t* bars, const DepSet& dep) {
+                             uint64_t* bars, const DepSet& dep, int L0, int L1) {
   const int lane = threadIdx.x & 31;
   const int C = a.C;
   const bool fin_on = a.st.stop_iter != nullptr;
-  const bool mirror_fin = fin_on && STOP;
-  int published = 0, granted = 0, issued = 0, fin_seen = 0;
+  SvcIter it;
+  it.r.init(L0, L1, a);
+  it.iter = 1;  // pass numbering (done[], grants) starts at sweep 1
+  it.c = 0;
+  it.fresh = true;
+  it.ended = false;
+  SBlock* const q = mb->q;  // generated blocks (at most 3 not done), ring by block number
+  int gen = 0, iss = 0, dn = 0;  // blocks generated / issued / done
+  int published = 0, fin_seen = 0, granted_k = 0;
   bool anystop = false;
+  // open partial: (plane, iteration) of the blocks summed so far
+  int acc_p = -1, acc_it = 0, slot_img = -1, slot_k = 0;
+  double acc = 0.0;
+  int acc_nf = 0;
+  auto flush = [&]() {
+    if (acc_p < 0) return;
+    if (lane == 0) {
+      const int img = acc_p / C;
+      if (img != slot_img) {  // the CTA's index within the image's range
+        slot_img = img;
+        slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(img) * a.pt.U));
+      }
+      const size_t slot = (size_t(acc_it % a.pt.ring) * a.P + acc_p) * a.pt.nbmax + slot_k;
+      a.pt.sum[slot] = acc;
+      a.pt.flag[slot] = acc_nf;
+    }
+    acc_p = -1;
+  };
   long long t0 = global_ns();
-  PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
-  PDZ_P(long long t_need = 0;)
   while (true) {
-    const bool last = ld_acquire_cta_shared(&mb->exit) != 0;  // before the counter:
-    const int x = ld_acquire_cta_shared(&mb->progress);      // it is final once `last`
-    const int seq = ld_acquire_cta_shared(&mb->req_seq);
-    const bool pub = x > published;
-    const bool want = seq > issued;
-    const LoadReq q = mb->req[(issued + 1) & 1];  // the next request, in order (valid if `want`)
-    bool grant = false;
-    if (want && q.k > granted) {
-      PDZ_P(if (t_need == 0) t_need = global_ns();)
-      const int n = (q.k - 1) / C + 1;
-      bool ok = true;
-      if (n >= 2) {
-        const int need = q.k - C;  // pass (n-1, c)
+    bool progressed = false;
+    // 1. blocks the compute warps finished (in order)
+    while (dn < iss && mbar_test(&bars[3 + (dn & 1)], uint32_t((dn >> 1) & 1))) {
+      const SBlock& b = q[dn & 3];
+      double s = 0.0;
+      int f = 0;
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-          for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
-            ok &= ld_relaxed(a.done + j) >= need;
+      for (int w = 0; w < kSCW; ++w) {
+        s += mb->red[dn & 1][w];
+        f |= mb->nf[dn & 1][w];
       }
-      PDZ_P(const bool ok_dep = __all_sync(0xffffffffu, ok);)
-      if (lane == 0 && fin_on) {
-        const int need_fin = STOP ? n - kNBuf : n - kRing;
-        if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
+      if (acc_p != b.p || acc_it != b.iter) {
+        flush();
+        acc_p = b.p;
+        acc_it = b.iter;
+        acc = 0.0;
+        acc_nf = 0;
       }
-      grant = __all_sync(0xffffffffu, ok);
-      PDZ_P(if (!ok_dep) sp[6] += 1; else if (!grant) sp[7] += 1;)
-      if (!grant && mirror_fin) grant = ld_relaxed(a.flags) != 0;  // every plane stopped
+      acc += s;
+      acc_nf |= f;
+      ++dn;
+      progressed = true;
+    }
+    // 2. generate the schedule ahead (at most 3 blocks not yet done)
+    bool wait_fin = false;
+    while (gen < dn + 3) {
+      SBlock nb;
+      const int k = it.template next<STOP>(a, nb, fin_seen, anystop);
+      if (k != kIterBlock) {
+        wait_fin = k == kIterWaitFin;
+        break;
+      }
+      if (lane == 0) q[gen & 3] = nb;
+      __syncwarp();
+      ++gen;
+    }
+    // the open partial is complete once no block of its (plane, iteration)
+    // is pending: the oldest pending block has another key, or everything
+    // generated is done and the iterator moved on (it is then at a pass start)
+    if (acc_p >= 0 && (dn < gen ? (q[dn & 3].p != acc_p || q[dn & 3].iter != acc_it)
+                                : (it.fresh || it.ended)))
+      flush();
+    // 3. progress: every pass before the oldest pending block is complete
+    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
+    const bool pub = upto > published;
+    // 4. grant for the next TMA load (block iss): neighbours, partial ring,
+    // buffer reuse (block iss - 2 done)
+    bool grant = false;
+    const bool want = iss < gen && iss < dn + 2;
+    if (want) {
+      const SBlock& b = q[iss & 3];
+      const int kpass = pass_index(b.iter, b.c, C);
+      if (kpass <= granted_k) {
+        grant = true;
+      } else {
+        bool ok = true;
+        if (b.iter >= 2) {
+          const int need = kpass - C;  // pass (n-1, c)
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
+              ok &= ld_relaxed(a.done + j) >= need;
+        }
+        if (lane == 0 && fin_on && !STOP) {
+          const int need_fin = b.iter - kRing;
+          if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
+        }
+        grant = __all_sync(0xffffffffu, ok);
+      }
     }
     int f = 0;
-    if (mirror_fin) f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
-    if (pub || grant || f > fin_seen || (want && q.k <= granted)) {
-      PDZ_P(const long long tf_ = global_ns();)
+    if (STOP && fin_on) f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
+    const bool fin_new = f > fin_seen;
+    if (pub || (grant && q[iss & 3].iter >= 2) || fin_new) {
       fence_acq_rel_gpu();  // release for the publication, acquire for the rest
-      PDZ_P(sp[0] += global_ns() - tf_; sp[1] += 1;)
       if (pub) {
-        if (lane == 0) st_relaxed(a.done + blockIdx.x, x);
-        published = x;
+        if (lane == 0) st_relaxed(a.done + blockIdx.x, upto);
+        published = upto;
       }
-      if (f > fin_seen) {
+      if (fin_new) {
         fin_seen = f;
-        if (!anystop && a.st.running[0] < a.P) {  // written before fin (finaliser)
-          anystop = true;
-          if (lane == 0) st_release_cta_shared(&mb->anystop, 1);
-        }
-        if (lane == 0) st_release_cta_shared(&mb->fin, f);
+        if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
       }
-      if (grant) {
-        granted = q.k;
-        PDZ_P(sp[4] += global_ns() - t_need; sp[5] += 1; t_need = 0;)
+      progressed = true;
+    }
+    if (grant) {
+      const SBlock& b = q[iss & 3];
+      granted_k = max(granted_k, pass_index(b.iter, b.c, C));
+      if (lane == 0) {
+        mb->desc[iss & 1] = b;
+        fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
+        issue_block<R>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
       }
-      if (want && q.k <= granted) {
-        if (lane == 0) {
-          fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
-          issue_block<R>(a, q, q.ib ? in1 : in0, &bars[q.ib]);
-          PDZ_P(sp[2] += global_ns() - q.t_post; sp[3] += 1;)
-        }
-        issued += 1;
+      ++iss;
+      progressed = true;
+    }
+    // 6. end of the stream: everything done and published
+    if (it.ended && dn == gen && iss == gen && published >= it.completed(a)) {
+      if (lane == 0) {
+        mb->desc[iss & 1].n = 0;
+        mbar_arrive(&bars[iss & 1]);  // completes the phase with no bytes
       }
+      return;
+    }
+    if (progressed) {
       t0 = global_ns();
       continue;
-    }
-    if (last) {
-      PDZ_P(if (a.prof && lane == 0) for (int i = 0; i < 8; ++i)
-                a.prof[(a.pt.G + 1 + blockIdx.x) * 16 + i] = sp[i];)
-      return;
     }
     if (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs) {
       if (lane == 0) atomicExch(a.flags + 1, 1);
       __trap();  // a dependency never arrived: fail the launch rather than hang
     }
-    __nanosleep(want ? 32 : 128);
+    __nanosleep(wait_fin || want ? 32 : 64);
   }
 }
 
@@ -659,10 +705,11 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   float* const hbuf = smem + 2 * Gm::IN_FLOATS;
   float* const sphi = hbuf + Gm::H_FLOATS;
   float* const slam = sphi + Gm::PL_FLOATS;
-  // bars[0..1]: IN double buffer; bars[2]: the block's Phi / lambda tiles
+  // bars[0..1]: IN double buffer; bars[2]: the block's Phi / lambda tiles;
+  // bars[3 + (b & 1)]: block b done (one arrival per compute warp; two
+  // barriers, as the compute warps may finish b and b + 1 before the service
+  // warp looks, which one barrier's phase parity could not tell apart)
   uint64_t* const bars = reinterpret_cast<uint64_t*>(slam + Gm::PL_FLOATS);
-  __shared__ double s_red[kSCW];
-  __shared__ int s_nf[kSCW];
   __shared__ Mailbox mb;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -670,12 +717,9 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
+    mbar_init(&bars[3], kSCW);
+    mbar_init(&bars[4], kSCW);
     mbar_fence_init();
-    mb.progress = 0;
-    mb.exit = 0;
-    mb.fin = 0;
-    mb.anystop = 0;
-    mb.req_seq = 0;
   }
   __syncthreads();
 
@@ -683,95 +727,47 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   constexpr int RP = Gm::RP;
   const int WP = W + 2 * kPadC;                          // padded iterate row
   const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
-  const int S = int(a.pt.S), G = a.pt.G;
-  const int L0 = int(part_start(a.pt, blockIdx.x));
-  const int L1 = int(part_start(a.pt, blockIdx.x + 1));
   if (blockIdx.x == a.pt.G) {  // the extra CTA: finaliser
     finalizer_cta(a);
     return;
   }
   if (warp == kSCW) {
-    service_loop<R, STOP>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R));
+    const int L0 = int(part_start(a.pt, blockIdx.x));
+    const int L1 = int(part_start(a.pt, blockIdx.x + 1));
+    service_loop<R, STOP>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R), L0, L1);
     return;
   }
-
-  FlatIter it;
-  it.r.init(L0, L1, a);
-  it.iter = 1;  // pass numbering (done[], grants) starts at sweep 1
-  it.c = 0;
-  it.fresh = true;
-  it.ended = false;
-  PDZ_P(it.grant_ns = 0;)
-  PDZ_P(long long pf[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};)
-  PDZ_P(long long tph = 0;)
-  PDZ_P(const long long tk0 = global_ns();)
 
   // thread roles for the vertical pass / update: column pair, kRPW-row group
   const int c = 2 * lane;      // strip-local output column of the pair
   const int j0 = warp * kRPW;  // block-local first row
-  uint32_t phase0 = 0, phase1 = 0, phase_pl = 0;
+  uint32_t ph_in = 0, ph_pl = 0;  // bit ib: phase of IN(ib)
   int ib = 0;
 
-  // the lead compute thread posts the TMA request for a block's input rows; the
-  // service warp issues it once the block's pass is granted
-  int req_seq = 0;
-  int slot_img = -1, slot_k = 0;  // partial-sum slot of this CTA in its current image
-  auto post = [&](const SBlock& b, int buf) {
-    if (tid == kLead) {
-      ++req_seq;
-      mb.req[req_seq & 1] = LoadReq{b.p, b.x0, b.yb, b.iter, buf, pass_index(b.iter, b.c, a.C)
-                                    PDZ_P(, global_ns())};
-      st_release_cta_shared(&mb.req_seq, req_seq);
-    }
-  };
-
-  SBlock cur, nxt;
-  bool have = it.template next<STOP>(a, cur, 0, &mb.progress, &mb.fin, &mb.anystop) == kBlock;
-  if (have) post(cur, 0);
-  double acc_r2 = 0.0;
-  float acc_nf = 0.0f;
-
-  // Per block b (two CTA barriers):
-  //   (block b-1 ended with a barrier: IN(b-1), H and the Phi / lambda tiles
-  //   are free)
-  //   -> post IN(b+1) (the service warp loads it once granted, overlapping
-  //      block b) and queue the Phi / lambda tiles of b (hidden by the H pass)
-  //   -> wait IN(b); blur its n + 2R rows into H
-  //   -> barrier; wait Phi / lambda
-  //   -> vertical pass + divergence + update
-  //   -> barrier; flush the plane partial / publish the pass.
-  while (have) {
-    PDZ_P(const long long tn_ = global_ns();)
-    const int nk = it.template next<STOP>(a, nxt, cur.iter, &mb.progress, &mb.fin, &mb.anystop);
-    PDZ_P(pf[12] += global_ns() - tn_;)
-    bool have_nxt = nk == kBlock;
-    float* const in_cur = ib ? in1 : in0;
-    float* const h_cur = hbuf;
-    uint64_t* const bar_cur = &bars[ib];
-    const int gx = cur.x0 + c;
-    const bool col_ok = gx < W;
-    float* __restrict__ uout_all = a.buf[cur.iter % kNBuf];
-
-    // (the previous block ended with a CTA barrier: IN(b-1), H and the
-    // Phi / lambda tiles are free)
-    PDZ_P(pf[6] += 1;)
-    if (have_nxt) post(nxt, ib ^ 1);
-    if (tid == kLead) {  // Phi / lambda tiles of this block (iteration invariant)
+  // Per block b: wait IN(b) (posted by the service warp with its descriptor);
+  // blur its n + 2R rows into H; barrier; wait Phi / lambda; vertical pass +
+  // divergence + update; report the warp's r^2 and arrive on "done"; barrier
+  // (H is reused by the next block).
+  while (true) {
+    mbar_wait(&bars[ib], (ph_in >> ib) & 1u);
+    ph_in ^= 1u << ib;
+    const SBlock cur = mb.desc[ib];
+    if (cur.n == 0) break;
+    // the block's Phi / lambda tiles (iteration invariant; the buffer is free
+    // since the previous block's closing barrier), hidden by the H pass
+    if (tid == kComputeThreads - 32) {
       mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
       tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
       tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
     }
-    PDZ_P(tph = global_ns();)
+    float* const in_cur = ib ? in1 : in0;
+    float* const h_cur = hbuf;
+    const int gx = cur.x0 + c;
+    const bool col_ok = gx < W;
+    float* __restrict__ uout_all = a.buf[cur.iter % kNBuf];
+    double acc_r2 = 0.0;
+    float acc_nf = 0.0f;
 
-    // ---- wait for this block's input rows
-    if (ib) {
-      PDZ_PT(3, mbar_wait(bar_cur, phase1));
-      phase1 ^= 1;
-    } else {
-      PDZ_PT(3, mbar_wait(bar_cur, phase0));
-      phase0 ^= 1;
-    }
-    PDZ_P(pf[11] += global_ns() - tph; tph = global_ns(); pf[14] += tph - tn_; const long long tdata = tph;)
     const int hn = cur.n + 2 * R;
     // ---- image borders (np.pad "symmetric", solver.py:235: -1-i <- i,
     // H+i <- H-1-i): nothing mirrored is stored globally and the pads of the
@@ -860,11 +856,9 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
       dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
     }
-    PDZ_P(pf[9] += global_ns() - tph;)
-    PDZ_PT(4, compute_bar());
-    mbar_wait(&bars[2], phase_pl);
-    phase_pl ^= 1;
-    PDZ_P(tph = global_ns();)
+    compute_bar();
+    mbar_wait(&bars[2], ph_pl);
+    ph_pl ^= 1;
 
     // ---- vertical pass (FFMA2 over the column pair), divergence, update
     if (j0 < cur.n) {
@@ -989,69 +983,20 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       acc_nf += nfp.x + nfp.y;
     }
 
-    PDZ_P(pf[10] += global_ns() - tph;)
-    // ---- flush the plane partial when the plane changes; publish the pass
-    const bool pass_end = !have_nxt || nxt.pass_start;
-    const bool flush = pass_end || nxt.p != cur.p;
-    if (flush) {
-      double s = warp_sum(acc_r2);
+    // ---- report the block: the warp's r^2 and non-finite flag, then done
+    {
+      const double s = warp_sum(acc_r2);
       const int nfw = __any_sync(0xffffffffu, !(acc_nf == 0.0f));
       if (lane == 0) {
-        s_red[warp] = s;
-        s_nf[warp] = nfw;
+        mb.red[ib][warp] = s;  // block parity == IN buffer index
+        mb.nf[ib][warp] = nfw;
+        mbar_arrive(&bars[3 + ib]);
       }
     }
-    // end of the block: every read of IN / H / Phi / lambda and every output
-    // store of the block precede this barrier (it also orders the pass's
-    // outputs before the progress flag)
-    PDZ_PT(5, compute_bar());
-    PDZ_P(pf[13] += global_ns() - tdata;)
-    if (flush) {
-      if (tid == kLead) {
-        double t = 0.0;
-        int f = 0;
-#pragma unroll
-        for (int w2 = 0; w2 < kSCW; ++w2) {
-          t += s_red[w2];
-          f |= s_nf[w2];
-        }
-        const int img = cur.p / a.C;
-        if (img != slot_img) {  // first CTA of the image: computed once per image
-          slot_img = img;
-          slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(img) * a.pt.U));
-        }
-        const int k = slot_k;
-        const size_t slot = (size_t(cur.iter % a.pt.ring) * a.P + cur.p) * a.pt.nbmax + k;
-        a.pt.sum[slot] = t;
-        a.pt.flag[slot] = f;
-        if (pass_end) {
-          // passes up to the next pass's predecessor are complete
-          const int done_to = have_nxt ? pass_index(nxt.iter, nxt.c, a.C) - 1 : it.completed(a);
-          st_release_cta_shared(&mb.progress, done_to);
-        }
-      }
-      acc_r2 = 0.0;
-      acc_nf = 0.0f;
-    }
-    if (nk == kDefer) {
-      PDZ_P(pf[7] += 1;)
-      // the next pass needs this CTA's own progress: published above (the
-      // flush barrier ordered every store of the pass); continue when idle
-      have_nxt = it.template next<STOP>(a, nxt, 0, &mb.progress, &mb.fin, &mb.anystop) == kBlock;
-      if (have_nxt) post(nxt, ib ^ 1);
-    }
-    cur = nxt;
-    have = have_nxt;
+    // every read of IN / H / Phi / lambda of the block precedes this barrier
+    // (H is rewritten by the next block's horizontal pass)
+    compute_bar();
     ib ^= 1;
-  }
-  if (tid == kLead) {
-    st_release_cta_shared(&mb.progress, pass_index(a.iter_last, a.C - 1, a.C));
-    st_release_cta_shared(&mb.exit, 1);
-    PDZ_P(if (a.prof) {
-      pf[0] = global_ns() - tk0;
-      pf[1] = it.grant_ns;
-      for (int i = 0; i < 16; ++i) a.prof[blockIdx.x * 16 + i] = pf[i];
-    })
   }
 }
 
