@@ -181,6 +181,11 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -451,6 +456,7 @@ struct Mailbox {
   SBlock q[4];           // service warp: generated blocks, ring by block number
   double red[2][kSCW];   // per-warp r^2 of block b in red[b & 1]
   int nf[2][kSCW];       // per-warp non-finite flag
+  PDZ_P(long long t_issue[2];)  // profiling: clock64 of IN(ib)'s TMA issue
 };
 
 // The service warp (warp kSCW) runs the CTA's whole schedule, so the compute
@@ -502,18 +508,19 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     acc_p = -1;
   };
   long long t0 = global_ns();
+  // [0] rounds [1] dependency-scan cycles [2] publications [3] sleeps
+  // [4] done events [5] cycles from a block's IN issue to its done being seen
+  PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0};)
   while (true) {
     bool progressed = false;
+    PDZ_P(sp[0] += 1;)
     // 1. blocks the compute warps finished (in order)
     while (dn < iss && mbar_test(&bars[3 + (dn & 1)], uint32_t((dn >> 1) & 1))) {
       const SBlock& b = q[dn & 3];
-      double s = 0.0;
-      int f = 0;
-#pragma unroll
-      for (int w = 0; w < kSCW; ++w) {
-        s += mb->red[dn & 1][w];
-        f |= mb->nf[dn & 1][w];
-      }
+      // lane w holds warp w's value; a fixed butterfly sums them (lane 0's
+      // result is the one stored: deterministic)
+      const double s = warp_sum(lane < kSCW ? mb->red[dn & 1][lane] : 0.0);
+      const int f = __any_sync(0xffffffffu, lane < kSCW && mb->nf[dn & 1][lane] != 0);
       if (acc_p != b.p || acc_it != b.iter) {
         flush();
         acc_p = b.p;
@@ -523,6 +530,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       }
       acc += s;
       acc_nf |= f;
+      PDZ_P(sp[4] += 1; sp[5] += clock64() - t_iss[dn & 3];)
       ++dn;
       progressed = true;
     }
@@ -545,59 +553,64 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     if (acc_p >= 0 && (dn < gen ? (q[dn & 3].p != acc_p || q[dn & 3].iter != acc_it)
                                 : (it.fresh || it.ended)))
       flush();
-    // 3. progress: every pass before the oldest pending block is complete
+    // 3a. progress, first (it unblocks the neighbours): every pass before the
+    // oldest pending block is complete; one release store (the block outputs
+    // the done barrier made visible to this warp, and the partials above)
     const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
-    const bool pub = upto > published;
-    // 4. grant for the next TMA load (block iss): neighbours, partial ring,
-    // buffer reuse (block iss - 2 done)
-    bool grant = false;
+    if (upto > published) {
+      if (lane == 0) st_release(a.done + blockIdx.x, upto);
+      PDZ_P(sp[2] += 1;)
+      published = upto;
+      progressed = true;
+    }
+    // 3b. grant for the next TMA load (block iss): neighbours' progress by
+    // acquire loads (no fence on this path), the partial ring, buffer reuse
+    // (block iss - 2 done)
     const bool want = iss < gen && iss < dn + 2;
     if (want) {
       const SBlock& b = q[iss & 3];
       const int kpass = pass_index(b.iter, b.c, C);
-      if (kpass <= granted_k) {
-        grant = true;
-      } else {
+      bool grant = kpass <= granted_k;
+      if (!grant) {
         bool ok = true;
+        PDZ_P(const long long ts = clock64();)
         if (b.iter >= 2) {
           const int need = kpass - C;  // pass (n-1, c)
 #pragma unroll
           for (int i = 0; i < 3; ++i)
             for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
-              ok &= ld_relaxed(a.done + j) >= need;
+              ok &= ld_acquire_gpu(a.done + j) >= need;
         }
-        if (lane == 0 && fin_on && !STOP) {
+        if (fin_on && !STOP) {
           const int need_fin = b.iter - kRing;
-          if (need_fin > 0) ok &= ld_relaxed(a.fin) >= need_fin;
+          if (need_fin > 0) ok &= ld_acquire_gpu(a.fin) >= need_fin;
         }
         grant = __all_sync(0xffffffffu, ok);
+        __syncwarp();  // every lane's acquire -> lane 0's TMA
+        PDZ_P(sp[1] += clock64() - ts;)
+      }
+      if (grant) {
+        granted_k = max(granted_k, kpass);
+        if (lane == 0) {
+          mb->desc[iss & 1] = b;
+          fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
+          issue_block<R>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
+          PDZ_P(mb->t_issue[iss & 1] = clock64();)
+        }
+        PDZ_P(t_iss[iss & 3] = clock64();)
+        ++iss;
+        progressed = true;
       }
     }
-    int f = 0;
-    if (STOP && fin_on) f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
-    const bool fin_new = f > fin_seen;
-    if (pub || (grant && q[iss & 3].iter >= 2) || fin_new) {
-      fence_acq_rel_gpu();  // release for the publication, acquire for the rest
-      if (pub) {
-        if (lane == 0) st_relaxed(a.done + blockIdx.x, upto);
-        published = upto;
-      }
-      if (fin_new) {
+    // 4. stop decisions (stop rule): fin by acquire load in every lane (all
+    // lanes read the stop records in the iterator)
+    if (STOP && fin_on) {
+      const int f = ld_acquire_gpu(a.fin);
+      if (f > fin_seen) {
         fin_seen = f;
         if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
+        progressed = true;
       }
-      progressed = true;
-    }
-    if (grant) {
-      const SBlock& b = q[iss & 3];
-      granted_k = max(granted_k, pass_index(b.iter, b.c, C));
-      if (lane == 0) {
-        mb->desc[iss & 1] = b;
-        fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
-        issue_block<R>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
-      }
-      ++iss;
-      progressed = true;
     }
     // 6. end of the stream: everything done and published
     if (it.ended && dn == gen && iss == gen && published >= it.completed(a)) {
@@ -605,6 +618,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         mb->desc[iss & 1].n = 0;
         mbar_arrive(&bars[iss & 1]);  // completes the phase with no bytes
       }
+      PDZ_P(if (a.prof && lane == 0) for (int i = 0; i < 8; ++i)
+                a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + i] = sp[i];)
       return;
     }
     if (progressed) {
@@ -615,6 +630,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       if (lane == 0) atomicExch(a.flags + 1, 1);
       __trap();  // a dependency never arrived: fail the launch rather than hang
     }
+    PDZ_P(sp[3] += 1;)
     __nanosleep(wait_fin || want ? 32 : 64);
   }
 }
@@ -743,6 +759,12 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   const int j0 = warp * kRPW;  // block-local first row
   uint32_t ph_in = 0, ph_pl = 0;  // bit ib: phase of IN(ib)
   int ib = 0;
+  // profile rows (PDZ_PROFILE builds): lane 0 of warps 0 and kSCW-1, clock64
+  // [0] total [1] IN wait [2] H pass [3] H barrier [4] Phi/lambda wait
+  // [5] V pass [6] report + end barrier [7] blocks
+  PDZ_P(long long pf[16] = {0}; const long long tk0 = clock64(); long long tq = tk0;)
+  // [8] waits that found the load not yet issued [9] sum of (issue - wait start)
+  // for those [10] waits on an issued load [11] sum of (ready - issue) for those
 
   // Per block b: wait IN(b) (posted by the service warp with its descriptor);
   // blur its n + 2R rows into H; barrier; wait Phi / lambda; vertical pass +
@@ -752,6 +774,14 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     mbar_wait(&bars[ib], (ph_in >> ib) & 1u);
     ph_in ^= 1u << ib;
     const SBlock cur = mb.desc[ib];
+    PDZ_P({
+      const long long t = clock64();
+      const long long ti = mb.t_issue[ib];
+      if (t - tq > 300) {  // actually waited
+        if (ti > tq) { pf[8] += 1; pf[9] += ti - tq; } else { pf[10] += 1; pf[11] += t - ti; }
+      }
+      pf[1] += t - tq; tq = t; pf[7] += 1;
+    })
     if (cur.n == 0) break;
     // the block's Phi / lambda tiles (iteration invariant; the buffer is free
     // since the previous block's closing barrier), hidden by the H pass
@@ -856,9 +886,12 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
       dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
     }
+    PDZ_P({ const long long t = clock64(); pf[2] += t - tq; tq = t; })
     compute_bar();
+    PDZ_P({ const long long t = clock64(); pf[3] += t - tq; tq = t; })
     mbar_wait(&bars[2], ph_pl);
     ph_pl ^= 1;
+    PDZ_P({ const long long t = clock64(); pf[4] += t - tq; tq = t; })
 
     // ---- vertical pass (FFMA2 over the column pair), divergence, update
     if (j0 < cur.n) {
@@ -983,6 +1016,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       acc_nf += nfp.x + nfp.y;
     }
 
+    PDZ_P({ const long long t = clock64(); pf[5] += t - tq; tq = t; })
     // ---- report the block: the warp's r^2 and non-finite flag, then done
     {
       const double s = warp_sum(acc_r2);
@@ -996,8 +1030,13 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     // every read of IN / H / Phi / lambda of the block precedes this barrier
     // (H is rewritten by the next block's horizontal pass)
     compute_bar();
+    PDZ_P({ const long long t = clock64(); pf[6] += t - tq; tq = t; })
     ib ^= 1;
   }
+  PDZ_P(if (a.prof && lane == 0 && (warp == 0 || warp == kSCW - 1)) {
+    pf[0] = clock64() - tk0;
+    for (int i = 0; i < 16; ++i) a.prof[(blockIdx.x * 2 + (warp != 0)) * 16 + i] = pf[i];
+  })
 }
 
 // ------------------------------------------------------------------- host --

@@ -1,5 +1,5 @@
-"""Per-CTA wait profile of the streaming solve (PDZ_PROF=1 debug build hook).
-usage: PDZ_PROF=1 prof_stream.py [size] [k] [iters]"""
+"""Per-CTA time profile of the persistent solve (PDZ_PROFILE build + PDZ_PROF=1).
+usage: PDZ_LIB_NAME=libpdz_prof.so PDZ_PROF=1 python tools/prof_stream.py [size] [k] [iters]"""
 import ctypes
 import os
 import sys
@@ -38,52 +38,35 @@ torch.cuda.synchronize()
 buf = np.zeros((8192, 16), dtype=np.int64)
 lib.pdz_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lib.pdz_debug_prof(buf.ctypes.data, 8192)
-G = int(((buf[:4096, 6] > 0) & (buf[:4096, 12] > 0)).sum())
-g = buf[:G]
-sv = buf[G + 1:2 * G + 1]
-names = ["total", "grant", "topbar", "mbar", "hbar", "flushbar", "blocks", "defers",
-         "mirror", "hpass", "vpass", "prefetch", "next", "compute", "towait"]
+G = int((buf[0:4096:2, 7] > 0).sum())
+w0 = buf[0:2 * G:2]
+wl = buf[1:2 * G:2]
+sv = buf[2 * G + 2:3 * G + 2]
+pv = buf[3 * G + 4:4 * G + 4]
 os.makedirs("gpurun_out", exist_ok=True)
-np.save("gpurun_out/prof_raw.npy", buf[:2 * G + 1])
-print(f"G={len(g)}  iters={iters}  per-sweep us (mean / min / max over CTAs):")
-for i, n in enumerate(names):
-    v = g[:, i] / iters if i in (6, 7) else g[:, i] / (1e3 * iters)
-    print(f"  {n:9s} {v.mean():8.3f} {v.min():8.3f} {v.max():8.3f}")
-snames = ["fence_ns", "fences", "post2issue", "issues", "grantlat", "waitwr_ns", "depfail", "store_ns"]
-print("service warp per sweep (mean / min / max):")
-for i, n in enumerate(snames):
-    v = sv[:, i] / iters
-    if i in (0, 2, 4, 5, 7):
-        v = v / 1e3
-    if i == 2:
-        v = sv[:, 2] / np.maximum(sv[:, 3], 1) / 1e3  # per issue
-    print(f"  {n:9s} {v.mean():8.3f} {v.min():8.3f} {v.max():8.3f}")
-print("  fence us each", (sv[:, 0].sum() / max(1, sv[:, 1].sum())) / 1e3)
-S = ((size + 63) // 64) * size
-order = np.argsort(g[:, 1])
-print("slowest CTAs (least grant wait): cta strip y0 y1 grant_us/sweep")
-for i in order[:12]:
-    L0, L1 = i * S // G, (i + 1) * S // G
-    print(f"  {i:4d} strip {L0 // size:2d} rows {L0 % size:4d}-{(L1 - 1) % size:4d}  " +
-          " ".join(f"{n}={g[i, j] / 1e3 / iters:6.2f}" for j, n in enumerate(names)
-                   if j not in (0, 6, 7)))
-print("fastest:")
-for i in order[-5:]:
-    L0, L1 = i * S // G, (i + 1) * S // G
-    print(f"  {i:4d} strip {L0 // size:2d} rows {L0 % size:4d}-{(L1 - 1) % size:4d}  " +
-          " ".join(f"{n}={g[i, j] / 1e3 / iters:6.2f}" for j, n in enumerate(names)
-                   if j not in (0, 6, 7)))
-print("slowest CTAs by vpass:")
-for i in np.argsort(-g[:, 10])[:16]:
-    L0, L1 = i * S // G, (i + 1) * S // G
-    print(f"  {i:4d} strip {L0 // size:2d} rows {L0 % size:4d}-{(L1 - 1) % size:4d}  "
-          f"vpass={g[i, 10] / 1e3 / iters:6.2f} hpass={g[i, 9] / 1e3 / iters:6.2f} "
-          f"mbar={g[i, 3] / 1e3 / iters:6.2f}")
-print("fastest by vpass:", ", ".join(f"{i}:{g[i, 10] / 1e3 / iters:.2f}" for i in np.argsort(g[:, 10])[:6]))
+np.save("gpurun_out/prof_raw.npy", buf[:4 * G + 4])
+names = ["total", "in_wait", "hpass", "hbar", "pl_wait", "vpass", "report+bar", "blocks"]
+per = lambda x: x / iters  # cycles per sweep
+print(f"G={G} iters={iters}  cycles per sweep (mean / min / max over CTAs)")
+for lab, arr in (("warp 0", w0), (f"warp last", wl)):
+    print(lab)
+    for i, n in enumerate(names):
+        v = per(arr[:, i].astype(float))
+        print(f"  {n:11s} {v.mean():9.1f} {v.min():9.1f} {v.max():9.1f}")
+sn = ["rounds", "scan_cyc", "publish", "sleeps", "done_ev", "iss2done"]
+print("service warp per sweep:")
+for i, n in enumerate(sn):
+    v = sv[:, i].astype(float) / iters
+    if i == 5:
+        v = sv[:, 5] / np.maximum(sv[:, 4], 1)
+    print(f"  {n:9s} {v.mean():9.1f} {v.min():9.1f} {v.max():9.1f}")
+busy = (w0[:, 2] + w0[:, 5]) / iters
+print("warp0 busy (h+v) per sweep: mean %.0f max %.0f (cta %d)" % (busy.mean(), busy.max(), busy.argmax()))
+for i in np.argsort(-(w0[:, 1] + w0[:, 4]))[:8]:
+    print(f"  most waiting cta {i}: in_wait {w0[i,1]/iters:.0f} pl_wait {w0[i,4]/iters:.0f} hbar {w0[i,3]/iters:.0f}")
+for i in np.argsort(w0[:, 1] + w0[:, 4])[:8]:
+    print(f"  least waiting cta {i}: in_wait {w0[i,1]/iters:.0f} pl_wait {w0[i,4]/iters:.0f} hbar {w0[i,3]/iters:.0f} vpass {w0[i,5]/iters:.0f}")
 
-print("per-CTA compute (data ready -> end barrier) and lead-warp wait (loop top -> data), us/sweep:")
-comp = g[:, 13] / 1e3 / iters
-wt = g[:, 14] / 1e3 / iters
-for i in np.argsort(-comp)[:20]:
-    print(f"  cta {i:4d} compute {comp[i]:6.2f}  wait {wt[i]:6.2f}  hpass {g[i, 9] / 1e3 / iters:5.2f} vpass {g[i, 10] / 1e3 / iters:5.2f}")
-print("compute: mean %.2f min %.2f max %.2f" % (comp.mean(), comp.min(), comp.max()))
+n8, s9, n10, s11 = (w0[:, 8].sum(), w0[:, 9].sum(), w0[:, 10].sum(), w0[:, 11].sum())
+print(f"warp0 waits: {n8/G/iters:.2f}/sweep found the load unissued (avg issue {s9/max(n8,1):.0f} cyc after wait start); "
+      f"{n10/G/iters:.2f}/sweep waited on an issued load (avg ready {s11/max(n10,1):.0f} cyc after issue)")
