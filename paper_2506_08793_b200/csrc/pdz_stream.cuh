@@ -60,7 +60,12 @@ constexpr int kRPW = 6;                     // output rows per compute warp
 constexpr int kSRB = kSCW * kRPW;           // output rows per block
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
-constexpr int kRing = 4;                    // partial-sum slots (iterations in flight)
+constexpr int kRing = 4;
+// A block's input rows arrive in two TMA boxes, rows [0, kSplit) and
+// [kSplit, ROWS), with their own mbarriers: the first wave of horizontal-pass
+// items (608 threads, 8-row groups) only touches rows < 80, so it starts as
+// soon as the first box lands.
+constexpr int kSplit = 80;                    // partial-sum slots (iterations in flight)
 constexpr int kNBuf = 3;                    // iterate buffers (iteration n in buf[n % 3])
 // Column pad of the padded iterates: 32 floats (128 B) each side, so padded
 // rows and every strip's first image column are 128-byte aligned (only the
@@ -89,6 +94,7 @@ struct StreamArgs {
   // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2 kPadC], box
   // {PITCH, kSRB + 2R, 1}.
   CUtensorMap tm[kNBuf];
+  CUtensorMap tm2[kNBuf];  // the same buffers, box {PITCH, ROWS - kSplit, 1} (second part)
   CUtensorMap tm_phi;   // Phi [P][H][W], box {64, kSRB, 1}
   CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, kSRB, 1}
   float* buf[kNBuf];   // iterate n in buf[n % kNBuf] (padded planes)
@@ -391,8 +397,12 @@ __device__ __forceinline__ void issue_block(const StreamArgs& a, const SBlock& q
                                             uint64_t* bar) {
   using Gm = SGeo<R>;
   const int buf = (q.iter - 1) % kNBuf;  // the buffer iteration `iter` reads
-  mbar_expect_tx(bar, uint32_t(Gm::ROWS) * Gm::PITCH * 4u);
+  static_assert(Gm::ROWS > kSplit, "two-part row load");
+  mbar_expect_tx(bar, uint32_t(kSplit) * Gm::PITCH * 4u);
   tma_load_3d(in, &a.tm[buf], q.x0 + kPadC - Gm::RP, q.yb, q.p, bar);
+  mbar_expect_tx(bar + 5, uint32_t(Gm::ROWS - kSplit) * Gm::PITCH * 4u);
+  tma_load_3d(in + kSplit * Gm::PITCH, &a.tm2[buf], q.x0 + kPadC - Gm::RP, q.yb + kSplit, q.p,
+              bar + 5);
 }
 
 // --------------------------------------------------------- service warp --
@@ -735,6 +745,8 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     mbar_init(&bars[2], 1);
     mbar_init(&bars[3], kSCW);
     mbar_init(&bars[4], kSCW);
+    mbar_init(&bars[5], 1);  // IN(0) rows >= kSplit
+    mbar_init(&bars[6], 1);  // IN(1) rows >= kSplit
     mbar_fence_init();
   }
   __syncthreads();
@@ -771,8 +783,10 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   // divergence + update; report the warp's r^2 and arrive on "done"; barrier
   // (H is reused by the next block).
   while (true) {
-    mbar_wait(&bars[ib], (ph_in >> ib) & 1u);
+    const uint32_t par = (ph_in >> ib) & 1u;
+    mbar_wait(&bars[ib], par);
     ph_in ^= 1u << ib;
+    bool got2 = false;  // second part of the rows (bars[5 + ib], same parity)
     const SBlock cur = mb.desc[ib];
     PDZ_P({
       const long long t = clock64();
@@ -830,6 +844,10 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       if (i >= hn) continue;
       const int y = ylo + i;  // a pad row reads its mirror source row
       const int si = (y < 0 ? -1 - y : (y >= H ? 2 * H - 1 - y : y)) - ylo;
+      if (!got2 && si >= kSplit) {
+        mbar_wait(&bars[5 + ib], par);
+        got2 = true;
+      }
       const float* row = in_cur + si * Gm::PITCH + 8 * g;
       constexpr int OFF = Gm::RP - R;
       constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
@@ -886,6 +904,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
       dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
     }
+    if (!got2) mbar_wait(&bars[5 + ib], par);  // the vertical pass reads every row
     PDZ_P({ const long long t = clock64(); pf[2] += t - tq; tq = t; })
     compute_bar();
     PDZ_P({ const long long t = clock64(); pf[3] += t - tq; tq = t; })

@@ -492,10 +492,16 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
   const cuuint64_t strides[2] = {wp * 4, wp * hp * 4};
   const cuuint32_t estr[3] = {1, 1, 1};
   for (int bi = 0; bi < kNBuf; ++bi) {
-    const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + kSRB), 1};
+    // two boxes per block: rows [0, kSplit) and [kSplit, 2R + kSRB)
+    const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(kSplit), 1};
+    const cuuint32_t box2[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + kSRB - kSplit), 1};
     CUresult r = encode(&b->tm[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+      r = encode(&b->tm2[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides, box2,
+                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
       return PDZ_ECUDA;
