@@ -30,6 +30,8 @@ cfg = pdz.SolverConfig(tau=tau, sigma=k / 6.0, kernel_size=k, max_iters=iters, r
 t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
 phi, lam = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg))
 prm = _params(size, size, chans, chans, cfg)
+if os.environ.get("PDZ_NOSTOP"):  # experiment: fixed iterations without the stop-rule machinery
+    prm.rel_tol = -1.0
 ws = torch.empty(lib.pdz_solve_workspace_bytes(prm), dtype=torch.uint8, device="cuda")
 for _ in range(3):
     nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(phi), nat.ptr(lam), nat.ptr(ws),
