@@ -119,6 +119,14 @@ struct StreamArgs {
 // Profiling instrumentation (tools/prof_stream.py): compiled only with
 // -DPDZ_PROFILE (build with PDZ_PROFILE=1), absent from the product build.
 #ifdef PDZ_PROFILE
+// timeline (ns, globaltimer): kind 0 progress >= k published, 1 pass k's IN
+// issued, 2 pass k's IN wanted (generated, buffer free), 3 / 4 compute warps
+// start / end waiting for pass k's IN
+#define PDZ_TL(a, kind, cta, k)                                                              \
+  do {                                                                                       \
+    if ((a).prof && (k) > 0 && (k) < 2048 && (cta) < 256)                                     \
+      (a).prof[131072 + ((size_t(kind) * 256 + (cta)) * 2048 + (k))] = global_ns();           \
+  } while (0)
 #define PDZ_P(...) __VA_ARGS__
 #define PDZ_PT(slot, stmt)            \
   {                                   \
@@ -495,6 +503,15 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   it.c = 0;
   it.fresh = true;
   it.ended = false;
+  // flattened dependency list: lane l checks CTAs #l and #l + 32 of the
+  // (disjoint) intervals; more than 64: the generic per-interval loop
+  int ndep = 0, dep0 = -1, dep1 = -1;
+  for (int i = 0; i < 3; ++i) {
+    const int n = dep.hi[i] >= dep.lo[i] ? dep.hi[i] - dep.lo[i] + 1 : 0;
+    if (lane >= ndep && lane < ndep + n) dep0 = dep.lo[i] + lane - ndep;
+    if (lane + 32 >= ndep && lane + 32 < ndep + n) dep1 = dep.lo[i] + lane + 32 - ndep;
+    ndep += n;
+  }
   SBlock* const q = mb->q;  // generated blocks (at most 3 not done), ring by block number
   int gen = 0, iss = 0, dn = 0;  // blocks generated / issued / done
   int published = 0, fin_seen = 0, granted_k = 0;
@@ -520,7 +537,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   long long t0 = global_ns();
   // [0] rounds [1] dependency-scan cycles [2] publications [3] sleeps
   // [4] done events [5] cycles from a block's IN issue to its done being seen
-  PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0};)
+  PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0}; int want_k = 0;)
   while (true) {
     bool progressed = false;
     PDZ_P(sp[0] += 1;)
@@ -551,6 +568,16 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       const int k = it.template next<STOP>(a, nb, fin_seen, anystop);
       if (k != kIterBlock) {
         wait_fin = k == kIterWaitFin;
+        if (wait_fin) {  // stop rule: the decisions of iteration n - 3 are needed
+          const int f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
+          if (f > fin_seen) {
+            fence_acq_rel_gpu();  // acquire: the stop records
+            fin_seen = f;
+            if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
+            progressed = true;
+            continue;  // retry the pass start
+          }
+        }
         break;
       }
       if (lane == 0) q[gen & 3] = nb;
@@ -563,62 +590,70 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     if (acc_p >= 0 && (dn < gen ? (q[dn & 3].p != acc_p || q[dn & 3].iter != acc_it)
                                 : (it.fresh || it.ended)))
       flush();
-    // 3a. progress, first (it unblocks the neighbours): every pass before the
-    // oldest pending block is complete; one release store (the block outputs
-    // the done barrier made visible to this warp, and the partials above)
+    // 3. scan for the next TMA load (block iss): relaxed loads of the
+    // neighbours' progress, one per lane (the flattened dependency list),
+    // issued before the publication's release so the two latencies overlap
+    const bool want = iss < gen && iss < dn + 2;
+    int kpass = 0, need = 0, need_fin = 0;
+    int v0 = 0x7fffffff, v1 = 0x7fffffff, vf = 0x7fffffff;
+    bool scan = false;
+    if (want) {
+      const SBlock& b = q[iss & 3];
+      kpass = pass_index(b.iter, b.c, C);
+      PDZ_P(if (lane == 0 && want_k != kpass) { want_k = kpass; PDZ_TL(a, 2, blockIdx.x, kpass); })
+      if (kpass > granted_k) {
+        scan = true;
+        need = kpass - C;  // pass (n-1, c)
+        if (b.iter >= 2) {
+          if (ndep <= 64) {
+            if (dep0 >= 0) v0 = ld_relaxed(a.done + dep0);
+            if (dep1 >= 0) v1 = ld_relaxed(a.done + dep1);
+          } else {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+              for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
+                ok &= ld_relaxed(a.done + j) >= need;
+            v0 = ok ? 0x7fffffff : -1;
+          }
+        }
+        need_fin = b.iter - kRing;
+        if (fin_on && !STOP && need_fin > 0 && lane == 0) vf = ld_relaxed(a.fin);
+      }
+    }
+    // 4. progress: every pass before the oldest pending block is complete;
+    // one release store (the block outputs the done barrier made visible to
+    // this warp, and the partials above)
     const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
     if (upto > published) {
       if (lane == 0) st_release(a.done + blockIdx.x, upto);
+      PDZ_P(if (lane == 0) for (int kk = published + 1; kk <= upto; ++kk)
+                PDZ_TL(a, 0, blockIdx.x, kk);)
       PDZ_P(sp[2] += 1;)
       published = upto;
       progressed = true;
     }
-    // 3b. grant for the next TMA load (block iss): neighbours' progress by
-    // acquire loads (no fence on this path), the partial ring, buffer reuse
-    // (block iss - 2 done)
-    const bool want = iss < gen && iss < dn + 2;
+    // 5. grant: every dependency met -> one acquire fence -> the TMA
     if (want) {
-      const SBlock& b = q[iss & 3];
-      const int kpass = pass_index(b.iter, b.c, C);
-      bool grant = kpass <= granted_k;
-      if (!grant) {
-        bool ok = true;
+      bool grant = !scan;
+      if (scan) {
         PDZ_P(const long long ts = clock64();)
-        if (b.iter >= 2) {
-          const int need = kpass - C;  // pass (n-1, c)
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-            for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
-              ok &= ld_acquire_gpu(a.done + j) >= need;
-        }
-        if (fin_on && !STOP) {
-          const int need_fin = b.iter - kRing;
-          if (need_fin > 0) ok &= ld_acquire_gpu(a.fin) >= need_fin;
-        }
+        const bool ok = v0 >= need && v1 >= need && (need_fin <= 0 || vf >= need_fin);
         grant = __all_sync(0xffffffffu, ok);
-        __syncwarp();  // every lane's acquire -> lane 0's TMA
+        if (grant) fence_acq_rel_gpu();  // acquire: the neighbours' rows
         PDZ_P(sp[1] += clock64() - ts;)
       }
       if (grant) {
+        const SBlock& b = q[iss & 3];
         granted_k = max(granted_k, kpass);
         if (lane == 0) {
           mb->desc[iss & 1] = b;
           fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
           issue_block<R>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
-          PDZ_P(mb->t_issue[iss & 1] = clock64();)
+          PDZ_P(mb->t_issue[iss & 1] = clock64(); PDZ_TL(a, 1, blockIdx.x, kpass);)
         }
         PDZ_P(t_iss[iss & 3] = clock64();)
         ++iss;
-        progressed = true;
-      }
-    }
-    // 4. stop decisions (stop rule): fin by acquire load in every lane (all
-    // lanes read the stop records in the iterator)
-    if (STOP && fin_on) {
-      const int f = ld_acquire_gpu(a.fin);
-      if (f > fin_seen) {
-        fin_seen = f;
-        if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
         progressed = true;
       }
     }
@@ -784,10 +819,18 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   // (H is reused by the next block).
   while (true) {
     const uint32_t par = (ph_in >> ib) & 1u;
+    PDZ_P(const long long tw0 = global_ns();)
     mbar_wait(&bars[ib], par);
     ph_in ^= 1u << ib;
     bool got2 = false;  // second part of the rows (bars[5 + ib], same parity)
     const SBlock cur = mb.desc[ib];
+    PDZ_P(if (tid == 0 && cur.n) {
+      const int kk = pass_index(cur.iter, cur.c, a.C);
+      if (a.prof && kk < 2048 && blockIdx.x < 256) {
+        a.prof[131072 + ((size_t(3) * 256 + blockIdx.x) * 2048 + kk)] = tw0;
+        PDZ_TL(a, 4, blockIdx.x, kk);
+      }
+    })
     PDZ_P({
       const long long t = clock64();
       const long long ti = mb.t_issue[ib];

@@ -604,7 +604,9 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   if (const char* e = getenv("PDZ_PROF")) {
     if (e[0] == '1' && pl.stream) {
       static long long* prof = nullptr;
-      if (!prof) cudaMalloc(&prof, 16 * 8192 * sizeof(long long));
+      // per-CTA stats rows [0, 8192) + timeline [5][256 CTAs][2048 passes] (ns)
+      if (!prof) cudaMalloc(&prof, 16 * 262144 * sizeof(long long));
+      if (prof) cudaMemset(prof, 0, 16 * 262144 * sizeof(long long));
       b.prof = prof;
       g_prof = prof;
     }
