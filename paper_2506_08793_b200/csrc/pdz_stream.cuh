@@ -122,11 +122,17 @@ struct StreamArgs {
 // timeline (ns, globaltimer): kind 0 progress >= k published, 1 pass k's IN
 // issued, 2 pass k's IN wanted (generated, buffer free), 3 / 4 compute warps
 // start / end waiting for pass k's IN
+#ifdef PDZ_TIMELINE
 #define PDZ_TL(a, kind, cta, k)                                                              \
   do {                                                                                       \
     if ((a).prof && (k) > 0 && (k) < 2048 && (cta) < 256)                                     \
       (a).prof[131072 + ((size_t(kind) * 256 + (cta)) * 2048 + (k))] = global_ns();           \
   } while (0)
+#else
+#define PDZ_TL(a, kind, cta, k) \
+  do {                          \
+  } while (0)
+#endif
 #define PDZ_P(...) __VA_ARGS__
 #define PDZ_PT(slot, stmt)            \
   {                                   \
@@ -514,7 +520,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   }
   SBlock* const q = mb->q;  // generated blocks (at most 3 not done), ring by block number
   int gen = 0, iss = 0, dn = 0;  // blocks generated / issued / done
-  int published = 0, fin_seen = 0, granted_k = 0;
+  int published = 0, fin_seen = 0, granted_k = 0, fin_probe = 0;
   bool anystop = false;
   // open partial: (plane, iteration) of the blocks summed so far
   int acc_p = -1, acc_it = 0, slot_img = -1, slot_k = 0;
@@ -538,9 +544,13 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   // [0] rounds [1] dependency-scan cycles [2] publications [3] sleeps
   // [4] done events [5] cycles from a block's IN issue to its done being seen
   PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0}; int want_k = 0;)
+  PDZ_P(long long tr = clock64(); long long rp[6] = {0, 0, 0, 0, 0, 0};)
+  // rp: cycles in [0] done events [1] generation [2] scan issue + publication
+  // [3] grant + TMA [4] sleeping [5] rest
   while (true) {
     bool progressed = false;
     PDZ_P(sp[0] += 1;)
+    PDZ_P(auto lap = [&](int i) { const long long t = clock64(); rp[i] += t - tr; tr = t; };)
     // 1. blocks the compute warps finished (in order)
     while (dn < iss && mbar_test(&bars[3 + (dn & 1)], uint32_t((dn >> 1) & 1))) {
       const SBlock& b = q[dn & 3];
@@ -561,6 +571,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       ++dn;
       progressed = true;
     }
+    PDZ_P(lap(0);)
     // 2. generate the schedule ahead (at most 3 blocks not yet done)
     bool wait_fin = false;
     while (gen < dn + 3) {
@@ -568,15 +579,14 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       const int k = it.template next<STOP>(a, nb, fin_seen, anystop);
       if (k != kIterBlock) {
         wait_fin = k == kIterWaitFin;
-        if (wait_fin) {  // stop rule: the decisions of iteration n - 3 are needed
-          const int f = __shfl_sync(0xffffffffu, lane == 0 ? ld_relaxed(a.fin) : 0, 0);
-          if (f > fin_seen) {
-            fence_acq_rel_gpu();  // acquire: the stop records
-            fin_seen = f;
-            if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
-            progressed = true;
-            continue;  // retry the pass start
-          }
+        // stop rule: the decisions of iteration n - 3 are needed; fin_probe
+        // was loaded at the end of the previous round (its latency hidden)
+        if (wait_fin && fin_probe > fin_seen) {
+          fence_acq_rel_gpu();  // acquire: the stop records
+          fin_seen = fin_probe;
+          if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
+          progressed = true;
+          continue;  // retry the pass start
         }
         break;
       }
@@ -590,6 +600,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     if (acc_p >= 0 && (dn < gen ? (q[dn & 3].p != acc_p || q[dn & 3].iter != acc_it)
                                 : (it.fresh || it.ended)))
       flush();
+    PDZ_P(lap(1);)
     // 3. scan for the next TMA load (block iss): relaxed loads of the
     // neighbours' progress, one per lane (the flattened dependency list),
     // issued before the publication's release so the two latencies overlap
@@ -621,6 +632,10 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         if (fin_on && !STOP && need_fin > 0 && lane == 0) vf = ld_relaxed(a.fin);
       }
     }
+    // stop rule: probe fin for the next round while the iterator waits for it
+    // (in flight together with the scan loads)
+    int fprobe = 0;
+    if (wait_fin && lane == 0) fprobe = ld_relaxed(a.fin);
     // 4. progress: every pass before the oldest pending block is complete;
     // one release store (the block outputs the done barrier made visible to
     // this warp, and the partials above)
@@ -633,6 +648,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       published = upto;
       progressed = true;
     }
+    PDZ_P(lap(2);)
     // 5. grant: every dependency met -> one acquire fence -> the TMA
     if (want) {
       bool grant = !scan;
@@ -657,26 +673,32 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         progressed = true;
       }
     }
+    if (wait_fin) fin_probe = __shfl_sync(0xffffffffu, fprobe, 0);
+    PDZ_P(lap(3);)
     // 6. end of the stream: everything done and published
     if (it.ended && dn == gen && iss == gen && published >= it.completed(a)) {
       if (lane == 0) {
         mb->desc[iss & 1].n = 0;
         mbar_arrive(&bars[iss & 1]);  // completes the phase with no bytes
       }
-      PDZ_P(if (a.prof && lane == 0) for (int i = 0; i < 8; ++i)
-                a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + i] = sp[i];)
+      PDZ_P(if (a.prof && lane == 0) {
+        for (int i = 0; i < 8; ++i) a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + i] = sp[i];
+        for (int i = 0; i < 6; ++i) a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + 8 + i] = rp[i];
+      })
       return;
     }
     if (progressed) {
       t0 = global_ns();
+      PDZ_P(lap(5);)
       continue;
     }
     if (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs) {
       if (lane == 0) atomicExch(a.flags + 1, 1);
       __trap();  // a dependency never arrived: fail the launch rather than hang
     }
-    PDZ_P(sp[3] += 1;)
+    PDZ_P(sp[3] += 1; lap(5);)
     __nanosleep(wait_fin || want ? 32 : 64);
+    PDZ_P(lap(4);)
   }
 }
 
