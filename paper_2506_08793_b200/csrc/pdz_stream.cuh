@@ -545,8 +545,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   // [4] done events [5] cycles from a block's IN issue to its done being seen
   PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0}; int want_k = 0;)
   PDZ_P(long long tr = clock64(); long long rp[6] = {0, 0, 0, 0, 0, 0};)
-  // rp: cycles in [0] done events [1] generation [2] scan issue + publication
-  // [3] grant + TMA [4] sleeping [5] rest
+  // rp: cycles in [0] done events [1] generation [2] scan [3] grant + TMA
+  // [4] sleeping [5] publication + rest
   while (true) {
     bool progressed = false;
     PDZ_P(sp[0] += 1;)
@@ -601,9 +601,9 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
                                 : (it.fresh || it.ended)))
       flush();
     PDZ_P(lap(1);)
-    // 3. scan for the next TMA load (block iss): relaxed loads of the
-    // neighbours' progress, one per lane (the flattened dependency list),
-    // issued before the publication's release so the two latencies overlap
+    // 3. scan for the next TMA load (block iss): acquire loads of the
+    // neighbours' progress, one per lane (the flattened dependency list; an
+    // acquire load is a strong load + L1 invalidation, no fence)
     const bool want = iss < gen && iss < dn + 2;
     int kpass = 0, need = 0, need_fin = 0;
     int v0 = 0x7fffffff, v1 = 0x7fffffff, vf = 0x7fffffff;
@@ -617,46 +617,35 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         need = kpass - C;  // pass (n-1, c)
         if (b.iter >= 2) {
           if (ndep <= 64) {
-            if (dep0 >= 0) v0 = ld_relaxed(a.done + dep0);
-            if (dep1 >= 0) v1 = ld_relaxed(a.done + dep1);
+            if (dep0 >= 0) v0 = ld_acquire_gpu(a.done + dep0);
+            if (dep1 >= 0) v1 = ld_acquire_gpu(a.done + dep1);
           } else {
             bool ok = true;
 #pragma unroll
             for (int i = 0; i < 3; ++i)
               for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
-                ok &= ld_relaxed(a.done + j) >= need;
+                ok &= ld_acquire_gpu(a.done + j) >= need;
             v0 = ok ? 0x7fffffff : -1;
           }
         }
         need_fin = b.iter - kRing;
-        if (fin_on && !STOP && need_fin > 0 && lane == 0) vf = ld_relaxed(a.fin);
+        if (fin_on && !STOP && need_fin > 0) vf = ld_acquire_gpu(a.fin);
       }
     }
     // stop rule: probe fin for the next round while the iterator waits for it
     // (in flight together with the scan loads)
     int fprobe = 0;
     if (wait_fin && lane == 0) fprobe = ld_relaxed(a.fin);
-    // 4. progress: every pass before the oldest pending block is complete;
-    // one release store (the block outputs the done barrier made visible to
-    // this warp, and the partials above)
-    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
-    if (upto > published) {
-      if (lane == 0) st_release(a.done + blockIdx.x, upto);
-      PDZ_P(if (lane == 0) for (int kk = published + 1; kk <= upto; ++kk)
-                PDZ_TL(a, 0, blockIdx.x, kk);)
-      PDZ_P(sp[2] += 1;)
-      published = upto;
-      progressed = true;
-    }
     PDZ_P(lap(2);)
-    // 5. grant: every dependency met -> one acquire fence -> the TMA
+    // 4. grant: every dependency met -> the TMA (before the publication, whose
+    // release fence would otherwise delay it)
     if (want) {
       bool grant = !scan;
       if (scan) {
         PDZ_P(const long long ts = clock64();)
         const bool ok = v0 >= need && v1 >= need && (need_fin <= 0 || vf >= need_fin);
         grant = __all_sync(0xffffffffu, ok);
-        if (grant) fence_acq_rel_gpu();  // acquire: the neighbours' rows
+        __syncwarp();  // every lane's acquire -> lane 0's TMA
         PDZ_P(sp[1] += clock64() - ts;)
       }
       if (grant) {
@@ -673,8 +662,21 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         progressed = true;
       }
     }
-    if (wait_fin) fin_probe = __shfl_sync(0xffffffffu, fprobe, 0);
     PDZ_P(lap(3);)
+    // 5. progress: every pass before the oldest pending block is complete;
+    // one release store (the block outputs the done barrier made visible to
+    // this warp, and the partials above)
+    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
+    if (upto > published) {
+      if (lane == 0) st_release(a.done + blockIdx.x, upto);
+      PDZ_P(if (lane == 0) for (int kk = published + 1; kk <= upto; ++kk)
+                PDZ_TL(a, 0, blockIdx.x, kk);)
+      PDZ_P(sp[2] += 1;)
+      published = upto;
+      progressed = true;
+    }
+    if (wait_fin) fin_probe = __shfl_sync(0xffffffffu, fprobe, 0);
+    PDZ_P(lap(5);)
     // 6. end of the stream: everything done and published
     if (it.ended && dn == gen && iss == gen && published >= it.completed(a)) {
       if (lane == 0) {

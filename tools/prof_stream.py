@@ -74,4 +74,4 @@ print(f"warp0 waits: {n8/G/iters:.2f}/sweep found the load unissued (avg issue {
       f"{n10/G/iters:.2f}/sweep waited on an issued load (avg ready {s11/max(n10,1):.0f} cyc after issue)")
 
 rp = sv[:, 8:14].astype(float) / iters
-print("service round cycles per sweep: done %.0f  gen %.0f  scan+publish %.0f  grant+tma %.0f  sleep %.0f  rest %.0f" % tuple(rp.mean(axis=0)))
+print("service round cycles per sweep: done %.0f  gen %.0f  scan %.0f  grant+tma %.0f  sleep %.0f  publish+rest %.0f" % tuple(rp.mean(axis=0)))
