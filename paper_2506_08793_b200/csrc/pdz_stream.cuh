@@ -830,6 +830,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   const int j0 = warp * kRPW;  // block-local first row
   uint32_t ph_in = 0, ph_pl = 0;  // bit ib: phase of IN(ib)
   int ib = 0;
+  int lam_img = -1, lam_yb = -1, lam_x0 = -1;  // rows of the lambda tile held
   // profile rows (PDZ_PROFILE builds): lane 0 of warps 0 and kSCW-1, clock64
   // [0] total [1] IN wait [2] H pass [3] H barrier [4] Phi/lambda wait
   // [5] V pass [6] report + end barrier [7] blocks
@@ -867,9 +868,18 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     // the block's Phi / lambda tiles (iteration invariant; the buffer is free
     // since the previous block's closing barrier), hidden by the H pass
     if (tid == kComputeThreads - 32) {
-      mbar_expect_tx(&bars[2], 2u * Gm::PL_FLOATS * 4u);
+      // the C channels of an image share lambda: kept while the block covers
+      // the same rows of the same image
+      const int img = cur.p / a.C;
+      const bool lam = img != lam_img || cur.yb != lam_yb || cur.x0 != lam_x0;
+      mbar_expect_tx(&bars[2], (lam ? 2u : 1u) * Gm::PL_FLOATS * 4u);
       tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
-      tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, cur.p / a.C, &bars[2]);
+      if (lam) {
+        tma_load_3d(slam, &a.tm_lam, cur.x0, cur.yb, img, &bars[2]);
+        lam_img = img;
+        lam_yb = cur.yb;
+        lam_x0 = cur.x0;
+      }
     }
     float* const in_cur = ib ? in1 : in0;
     float* const h_cur = hbuf;
