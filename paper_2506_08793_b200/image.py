@@ -132,3 +132,38 @@ def to_host(t, like) -> object:
         torch.cuda.current_stream(t.device).synchronize()
         return out
     return t.detach().to("cpu").numpy().astype(np.float64, copy=False)
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def to_host_async(t, like):
+    """Start `to_host(t, like)` now, on a side stream after the work queued so
+    far, so the copy overlaps later GPU work (dehaze: the transmission map and
+    airlight while the solve runs).  Returns a callable that waits and gives
+    the same value `to_host` would."""
+    if is_device_array(like) and like.is_cuda:
+        return lambda: t
+    import torch
+
+    dev = t.device
+    side = _SIDE_STREAMS.get(dev)
+    if side is None:
+        side = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    ready = torch.cuda.Event()
+    ready.record(torch.cuda.current_stream(dev))
+    out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        out.copy_(t, non_blocking=True)
+        t.record_stream(side)  # keep the device buffer alive until the copy ran
+        done = torch.cuda.Event()
+        done.record(side)
+
+    def finish():
+        done.synchronize()
+        if is_device_array(like):
+            return out
+        return out.numpy()  # float64 view of the page-locked copy
+
+    return finish

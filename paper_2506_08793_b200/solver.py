@@ -28,9 +28,8 @@ import numpy as np
 from . import _native as nat
 from .config import (ABLATIONS, LAMBDA_MODES, DehazeResult, SolverConfig, SolverTrace,
                      normalize_ablation)
-from .image import (clamp01, is_device_array, to_device, to_host, validate_field,
-                    validate_unit_image,
-                    validate_image)
+from .image import (clamp01, is_device_array, to_device, to_host, to_host_async,
+                    validate_field, validate_image, validate_unit_image)
 from .refine import refine_dev
 from .scattering import _airlight_dev, _blend_weights, _dark_dev, _device_vec, _unit_range
 
@@ -464,12 +463,14 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
         raise ValueError(f"field must be at least 2x2, got {(h, w)}")
     phi, lam, bounds = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg,
                                        _lambda_mode(flags, cfg), with_bounds=True)
+    # the transmission map and airlight are final: copy them out while the
+    # solve runs
+    t_host, a_host = to_host_async(t_dev, image), to_host_async(a_dev, image)
     problem = DeviceProblem(phi, lam, h, w, c, c, bounds)
     u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
     nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1, nat.stream_ptr()))
-    return (to_host(out, image),
-            DehazeResult(to_host(a_dev, image), to_host(t_dev, image), traces, flags))
+    return (to_host(out, image), DehazeResult(a_host(), t_host(), traces, flags))
 
 
 def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
