@@ -322,8 +322,11 @@ def run_gpu(args):
         t = torch.tensor([e2e_ms], device=phi.device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
+    # host reads per step: the restored image (H, W, C) f64, the transmission
+    # map (H, W) f64 and the airlight (C,) f64 of DehazeResult
     e2e = {"value": world * H * W * ITERS / (e2e_ms / 1e3) / 1e6, "unit": UNIT,
-           "h2d_bytes_per_step": H * W * C * 4, "d2h_bytes_per_step": H * W * C * 8,
+           "h2d_bytes_per_step": H * W * C * 4,
+           "d2h_bytes_per_step": H * W * C * 8 + H * W * 8 + C * 8,
            "ms_per_step": e2e_ms}
 
     cpu = None
