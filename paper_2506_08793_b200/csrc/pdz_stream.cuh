@@ -56,8 +56,10 @@ namespace pdz {
 
 constexpr int kSTW = 64;                    // strip width (output columns)
 constexpr int kSCW = 19;                    // compute warps (+1: 640 threads x 96 regs)
-constexpr int kRPW = 6;                     // output rows per compute warp
-constexpr int kSRB = kSCW * kRPW;           // output rows per block
+// Output rows per compute warp / per block: 6 / 114 up to R = 12; wider
+// halos (R = 24, K = 49) stage 4 / 76 rows so the buffers fit shared memory.
+__host__ __device__ constexpr int stream_rpw(int R) { return R <= 12 ? 6 : 4; }
+__host__ __device__ constexpr int stream_srb(int R) { return kSCW * stream_rpw(R); }
 constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
 constexpr int kComputeThreads = kSCW * 32;
 constexpr int kRing = 4;
@@ -78,25 +80,27 @@ constexpr long long kSpinTimeoutNs = 10000000000ll;
 // column group hit 8 distinct bank quads (conflict-free LDS.128 / STS.128).
 template <int R>
 struct SGeo {
+  static constexpr int RPW = stream_rpw(R);    // output rows per compute warp
+  static constexpr int SRB = stream_srb(R);    // output rows per block
   static constexpr int RP = (R + 3) & ~3;      // column halo rounded to float4
   static constexpr int PWD = kSTW + 2 * RP;    // staged floats per row used (even # float4)
   static constexpr int PITCH = PWD + 4;        // staged row pitch = TMA box width
   static constexpr int HP = kSTW + 4;          // H row pitch
-  static constexpr int ROWS = kSRB + 2 * R;    // staged input rows / H rows = TMA box height
+  static constexpr int ROWS = SRB + 2 * R;     // staged input rows / H rows = TMA box height
   static constexpr int IN_FLOATS = (ROWS * PITCH + 31) & ~31;  // 128-byte aligned buffers
   static constexpr int H_FLOATS = (ROWS * HP + 31) & ~31;
-  static constexpr int PL_FLOATS = kSRB * kSTW;  // Phi or lambda tile of the block
+  static constexpr int PL_FLOATS = SRB * kSTW;  // Phi or lambda tile of the block
   static constexpr size_t SMEM = size_t(2 * IN_FLOATS + H_FLOATS + 2 * PL_FLOATS) * 4 + 128;
   static constexpr bool FITS = SMEM <= 227 * 1024;
 };
 
 struct StreamArgs {
   // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2 kPadC], box
-  // {PITCH, kSRB + 2R, 1}.
+  // {PITCH, SRB + 2R, 1}.
   CUtensorMap tm[kNBuf];
   CUtensorMap tm2[kNBuf];  // the same buffers, box {PITCH, ROWS - kSplit, 1} (second part)
-  CUtensorMap tm_phi;   // Phi [P][H][W], box {64, kSRB, 1}
-  CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, kSRB, 1}
+  CUtensorMap tm_phi;   // Phi [P][H][W], box {64, SRB, 1}
+  CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, SRB, 1}
   float* buf[kNBuf];   // iterate n in buf[n % kNBuf] (padded planes)
   const float* phi;
   const float* lam;
@@ -107,6 +111,7 @@ struct StreamArgs {
   int32_t* flags;       // [0] iteration by which every plane stopped, [1] abort
   int32_t H, W, P, C, nstrips;
   int32_t iter_last, max_iters;  // sweeps 1..iter_last
+  int32_t srb;          // output rows per block (stream_srb(R))
   int32_t stop_rule;    // rel_tol active: pass (n, c) needs fin >= n - 2
   float eps, tau;
   double rel_tol;
@@ -339,7 +344,7 @@ struct RangeIter {
       blk.p = p;
       blk.x0 = s * kSTW;
       blk.yb = y;
-      blk.n = min(kSRB, seg_end - L);
+      blk.n = min(a.srb, seg_end - L);
       L += blk.n;
       y += blk.n;
       if (y == a.H) wrap(a);
@@ -827,6 +832,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
 
   // thread roles for the vertical pass / update: column pair, kRPW-row group
   const int c = 2 * lane;      // strip-local output column of the pair
+  constexpr int kRPW = Gm::RPW;
   const int j0 = warp * kRPW;  // block-local first row
   uint32_t ph_in = 0, ph_pl = 0;  // bit ib: phase of IN(ib)
   int ib = 0;
@@ -903,10 +909,11 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     const bool rbord = wl == kSTW;
     if (wl != kSTW && wl < kSTW + Gm::RP) {  // CTA-uniform
       const int xr = Gm::RP + wl;  // staged column of image column W
-      const int k = tid & 15;
-      static_assert(Gm::RP <= 16, "pad columns per row slot");
+      constexpr int SL = Gm::RP <= 16 ? 16 : 32;  // pad-column slots per row
+      static_assert(Gm::RP <= SL, "pad columns per row slot");
+      const int k = tid % SL;
       if (k < Gm::RP && xr + k < Gm::PWD)
-        for (int sr = tid >> 4; sr < hn; sr += kComputeThreads / 16)
+        for (int sr = tid / SL; sr < hn; sr += kComputeThreads / SL)
           in_cur[sr * Gm::PITCH + xr + k] = in_cur[sr * Gm::PITCH + xr - 1 - k];
       compute_bar();
     }
@@ -937,12 +944,26 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
       }
-      // pad columns in registers: left (staged column t < RP of group 0)
-      // <- 2 RP - 1 - t; right (full last strip, staged column 8g + t >= RP +
-      // 64) <- 2 RP + 127 - 8g - t.  Compile-time indices per group.
-      if (lbord && g == 0) {
+      // pad columns in registers, compile-time indices per group: left
+      // (staged column 8g + t < RP) <- 2 RP - 1 - 8g - t, in the groups that
+      // reach it (8g + OFF < RP, i.e. g < R / 8); right (full last strip,
+      // staged column 8g + t >= RP + 64) <- 2 RP + 127 - 8g - t.
+      if (lbord && 8 * g + OFF < Gm::RP) {
+        auto lpatch = [&](auto gtag) {
+          constexpr int GG = decltype(gtag)::value;
 #pragma unroll
-        for (int t = OFF; t < Gm::RP; ++t) v[t] = v[2 * Gm::RP - 1 - t];
+          for (int t = OFF; t < OFF + 2 * R + 8; ++t) {
+            const int tp = 2 * Gm::RP - 1 - 16 * GG - t;
+            if (8 * GG + t < Gm::RP && tp >= 0 && tp < 4 * NQ) v[t] = v[tp];
+          }
+        };
+        static_assert(R < 24 || Gm::RP <= 24, "left patch covers groups 0..2");
+        if (g == 0)
+          lpatch(std::integral_constant<int, 0>{});
+        else if (g == 1)
+          lpatch(std::integral_constant<int, 1>{});
+        else
+          lpatch(std::integral_constant<int, 2>{});
       }
       if (rbord && g >= 5) {
         auto patch = [&](auto gtag) {
@@ -1160,6 +1181,7 @@ static StreamFn stream_pick_stop(int R, size_t* smem) {
     case 6: return stream_prepared<6, EDGE, STOP>(smem);
     case 9: return stream_prepared<9, EDGE, STOP>(smem);
     case 12: return stream_prepared<12, EDGE, STOP>(smem);
+    case 24: return stream_prepared<24, EDGE, STOP>(smem);
     default: return nullptr;
   }
 }

@@ -492,9 +492,9 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
   const cuuint64_t strides[2] = {wp * 4, wp * hp * 4};
   const cuuint32_t estr[3] = {1, 1, 1};
   for (int bi = 0; bi < kNBuf; ++bi) {
-    // two boxes per block: rows [0, kSplit) and [kSplit, 2R + kSRB)
+    // two boxes per block: rows [0, kSplit) and [kSplit, 2R + SRB)
     const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(kSplit), 1};
-    const cuuint32_t box2[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + kSRB - kSplit), 1};
+    const cuuint32_t box2[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + stream_srb(R) - kSplit), 1};
     CUresult r = encode(&b->tm[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -507,13 +507,13 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
       return PDZ_ECUDA;
     }
   }
-  // Phi [P][H][W] and lambda [P / C][H][W] (dense), box {64, kSRB, 1}
+  // Phi [P][H][W] and lambda [P / C][H][W] (dense), box {64, SRB, 1}
   const cuuint64_t ddims[2][3] = {
       {cuuint64_t(p->width), cuuint64_t(p->height), cuuint64_t(p->planes)},
       {cuuint64_t(p->width), cuuint64_t(p->height), cuuint64_t(p->planes / p->channels)}};
   const cuuint64_t dstrides[2] = {cuuint64_t(p->width) * 4,
                                   cuuint64_t(p->width) * p->height * 4};
-  const cuuint32_t dbox[3] = {cuuint32_t(kSTW), cuuint32_t(kSRB), 1};
+  const cuuint32_t dbox[3] = {cuuint32_t(kSTW), cuuint32_t(stream_srb(R)), 1};
   const float* dsrc[2] = {phi, lam};
   CUtensorMap* dmap[2] = {&b->tm_phi, &b->tm_lam};
   for (int k = 0; k < 2; ++k) {
@@ -615,6 +615,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.eps = float(p->epsilon);
   b.tau = float(p->tau);
   b.rel_tol = p->rel_tol;
+  b.srb = stream_srb(pl.R);
   memcpy(b.w, w, sizeof(w));
   for (int i = 0; i < kMaxTaps; ++i) b.w2[i] = make_float2(w[i], w[i]);
   for (int i = 0; i <= kMaxTaps; ++i)
@@ -669,18 +670,27 @@ __global__ void sync_init_kernel(Sync sy, int G) {
   }
 }
 
-// u0 = Phi into a (possibly padded) iterate buffer: pads get the symmetric
-// reflection (solver.py:235) -- one fold, pads <= the image size.
-__global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict__ buf, int H,
-                                int W, int P, int pr, int pc) {
+// u0 = Phi into a (possibly padded) iterate buffer.  The persistent kernel's
+// readers reflect image borders themselves, so the pads of every iterate
+// buffer are poisoned with NaN: a read of a pad as data would surface as a
+// non-finite result instead of a silent error.
+__global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict__ buf,
+                                float* __restrict__ buf1, float* __restrict__ buf2, int H, int W,
+                                int P, int pr, int pc) {
   const int wp = W + 2 * pc, hp = H + 2 * pr;
   const int64_t n = int64_t(P) * hp * wp;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pl = i / (int64_t(hp) * wp);
-    const int r = int((i / wp) % hp), q = int(i % wp);
-    const int y = reflect(r - pr, H), x = reflect(q - pc, W);
-    buf[i] = phi[(pl * H + y) * W + x];
+    const int y = int((i / wp) % hp) - pr, x = int(i % wp) - pc;
+    if (y >= 0 && y < H && x >= 0 && x < W) {
+      buf[i] = phi[(pl * H + y) * W + x];
+    } else {
+      const float nan = __int_as_float(0x7fc00000);
+      buf[i] = nan;
+      if (buf1) buf1[i] = nan;
+      if (buf2) buf2[i] = nan;
+    }
   }
 }
 
@@ -832,8 +842,8 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   {
     const int64_t n = int64_t(p->planes) * (p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
-    pad_init_kernel<<<blocks, 256, 0, s>>>(phi, L.buf0, p->height, p->width, p->planes, pl.pad_r,
-                                           pl.pad_c);
+    pad_init_kernel<<<blocks, 256, 0, s>>>(phi, L.buf0, pl.stream ? L.buf1 : nullptr, L.buf2,
+                                           p->height, p->width, p->planes, pl.pad_r, pl.pad_c);
     PDZ_CHECK_LAUNCH("u0 = Phi");
   }
   init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);

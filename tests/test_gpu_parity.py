@@ -340,7 +340,10 @@ def test_batch_equals_single(pdz):
                                      # streaming kernel: partial last strip (W % 64 != 0),
                                      # full border strips at every compiled radius
                                      ((96, 100), 19), ((50, 68), 25), ((80, 132), 13),
-                                     ((72, 128), 25), ((40, 192), 5), ((36, 64), 7)])
+                                     ((72, 128), 25), ((40, 192), 5), ((36, 64), 7),
+                                     # K = 49 (R = 24, 76-row blocks): full strips, and
+                                     # partial strips whose halo crosses W
+                                     ((128, 192), 49), ((100, 136), 49)])
 def test_odd_shapes_against_oracle(pdz, shape, k):
     rng = np.random.default_rng(sum(shape) + k)
     ch = rng.random(shape) * 0.8 + 0.1
@@ -349,6 +352,25 @@ def test_odd_shapes_against_oracle(pdz, shape, k):
                            max_iters=25, rel_tol=1e-300)
     u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg)
     ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg), separable=True)
+    assert np.max(np.abs(u - ru)) <= U_TOL
+    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
+
+
+@pytest.mark.parametrize("shape,k", [((96, 128), 19), ((80, 132), 25), ((128, 192), 49),
+                                     ((100, 136), 49), ((70, 100), 13)])
+def test_border_sensitive_no_edge(pdz, shape, k):
+    # tau = 0.05 (D == 1 keeps it contractive) makes every border term ~200x
+    # more visible than at TAU_STABLE; the iterate pads are NaN-poisoned, so a
+    # pad read as data fails loudly
+    rng = np.random.default_rng(7 * k + shape[1])
+    ch = rng.random(shape) * 0.8 + 0.1
+    t = 0.3 + 0.6 * rng.random(shape)
+    cfg = pdz.SolverConfig(tau=0.05, kernel_size=k, sigma=max(1.0, k / 6.0), max_iters=12,
+                           rel_tol=1e-300)
+    u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg, edge_preserving=False)
+    ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg),
+                                edge_preserving=False, separable=True)
+    assert np.all(np.isfinite(u))
     assert np.max(np.abs(u - ru)) <= U_TOL
     np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
 
