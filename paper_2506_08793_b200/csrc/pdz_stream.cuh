@@ -55,19 +55,29 @@
 namespace pdz {
 
 constexpr int kSTW = 64;                    // strip width (output columns)
-constexpr int kSCW = 19;                    // compute warps (+1: 640 threads x 96 regs)
-// Output rows per compute warp / per block: 6 / 114 up to R = 12; wider
-// halos (R = 24, K = 49) stage 4 / 76 rows so the buffers fit shared memory.
-__host__ __device__ constexpr int stream_rpw(int R) { return R <= 12 ? 6 : 4; }
-__host__ __device__ constexpr int stream_srb(int R) { return kSCW * stream_rpw(R); }
-constexpr int kSThreads = (kSCW + 1) * 32;  // + service warp
-constexpr int kComputeThreads = kSCW * 32;
+// Block geometry V (a template parameter of the kernel, picked per solve from
+// the partition, pdz_sweep.cu):
+//  V = 0: 19 compute warps x 6 output rows (114-row blocks; 4 rows / 76 for
+//         R = 24, whose wider staging would not fit shared memory otherwise),
+//         20 warps x 96 registers (5 warps per SM sub-partition fill its
+//         16K-register file).  Best when a CTA's rows of a strip fit one block
+//         (config 2: ~114 rows per CTA).
+//  V = 1: 15 compute warps x 8 rows (120-row blocks) at 128 registers (4 warps
+//         per sub-partition), for CTAs that walk several blocks per pass
+//         (configs 3 and 4): fewer blocks per strip and more registers per
+//         thread for the vertical pass.
+__host__ __device__ constexpr int geo_scw(int V) { return V ? 15 : 19; }
+__host__ __device__ constexpr int geo_rpw(int R, int V) { return V ? 8 : (R <= 12 ? 6 : 4); }
+__host__ __device__ constexpr int geo_srb(int R, int V) { return geo_scw(V) * geo_rpw(R, V); }
+__host__ __device__ constexpr int geo_threads(int V) { return (geo_scw(V) + 1) * 32; }  // + service warp
+__host__ __device__ constexpr int geo_nreg(int V) { return V ? 128 : 96; }
+// A block's input rows arrive in two TMA boxes, rows [0, split) and
+// [split, ROWS), with their own mbarriers: the first wave of horizontal-pass
+// items (one per compute thread, 8-row groups) only touches rows < split, so
+// it starts as soon as the first box lands.
+__host__ __device__ constexpr int geo_split(int V) { return (geo_scw(V) * 32 / 64) * 8 + 8; }
+constexpr int kSCWMax = 19;                 // mailbox slots
 constexpr int kRing = 4;
-// A block's input rows arrive in two TMA boxes, rows [0, kSplit) and
-// [kSplit, ROWS), with their own mbarriers: the first wave of horizontal-pass
-// items (608 threads, 8-row groups) only touches rows < 80, so it starts as
-// soon as the first box lands.
-constexpr int kSplit = 80;                    // partial-sum slots (iterations in flight)
 constexpr int kNBuf = 3;                    // iterate buffers (iteration n in buf[n % 3])
 // Column pad of the padded iterates: 32 floats (128 B) each side, so padded
 // rows and every strip's first image column are 128-byte aligned (only the
@@ -78,10 +88,14 @@ constexpr long long kSpinTimeoutNs = 10000000000ll;
 // Shared-memory row pitches are an ODD number of float4s, so the 8 lanes of a
 // quarter-warp that read / write 16 bytes each in 8 different rows of the same
 // column group hit 8 distinct bank quads (conflict-free LDS.128 / STS.128).
-template <int R>
+template <int R, int V>
 struct SGeo {
-  static constexpr int RPW = stream_rpw(R);    // output rows per compute warp
-  static constexpr int SRB = stream_srb(R);    // output rows per block
+  static constexpr int SCW = geo_scw(V);       // compute warps
+  static constexpr int CT = SCW * 32;          // compute threads
+  static constexpr int NT = geo_threads(V);    // threads per CTA
+  static constexpr int SPLIT = geo_split(V);   // rows of the first TMA box
+  static constexpr int RPW = geo_rpw(R, V);    // output rows per compute warp
+  static constexpr int SRB = geo_srb(R, V);    // output rows per block
   static constexpr int RP = (R + 3) & ~3;      // column halo rounded to float4
   static constexpr int PWD = kSTW + 2 * RP;    // staged floats per row used (even # float4)
   static constexpr int PITCH = PWD + 4;        // staged row pitch = TMA box width
@@ -98,7 +112,7 @@ struct StreamArgs {
   // TMA maps of the two padded iterate buffers [P][H + 2R][W + 2 kPadC], box
   // {PITCH, SRB + 2R, 1}.
   CUtensorMap tm[kNBuf];
-  CUtensorMap tm2[kNBuf];  // the same buffers, box {PITCH, ROWS - kSplit, 1} (second part)
+  CUtensorMap tm2[kNBuf];  // the same buffers, box {PITCH, ROWS - SPLIT, 1} (second part)
   CUtensorMap tm_phi;   // Phi [P][H][W], box {64, SRB, 1}
   CUtensorMap tm_lam;   // lambda [P / C][H][W], box {64, SRB, 1}
   float* buf[kNBuf];   // iterate n in buf[n % kNBuf] (padded planes)
@@ -111,7 +125,7 @@ struct StreamArgs {
   int32_t* flags;       // [0] iteration by which every plane stopped, [1] abort
   int32_t H, W, P, C, nstrips;
   int32_t iter_last, max_iters;  // sweeps 1..iter_last
-  int32_t srb;          // output rows per block (stream_srb(R))
+  int32_t srb;          // output rows per block (geo_srb(R, V))
   int32_t stop_rule;    // rel_tol active: pass (n, c) needs fin >= n - 2
   float eps, tau;
   double rel_tol;
@@ -230,8 +244,9 @@ __device__ __forceinline__ long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+template <int CT>
 __device__ __forceinline__ void compute_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
 }
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
@@ -411,10 +426,11 @@ struct SvcIter {
 // yb - R + i (padded row yb + i); rows beyond the block's n + 2R are
 // over-fetch, never read.  Pad rows / columns of the box are reflected by
 // the readers (the pads of the iterates carry no data).
-template <int R>
+template <int R, int V>
 __device__ __forceinline__ void issue_block(const StreamArgs& a, const SBlock& q, float* in,
                                             uint64_t* bar) {
-  using Gm = SGeo<R>;
+  using Gm = SGeo<R, V>;
+  constexpr int kSplit = Gm::SPLIT;
   const int buf = (q.iter - 1) % kNBuf;  // the buffer iteration `iter` reads
   static_assert(Gm::ROWS > kSplit, "two-part row load");
   mbar_expect_tx(bar, uint32_t(kSplit) * Gm::PITCH * 4u);
@@ -483,12 +499,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 struct Mailbox {
   SBlock desc[2];        // block of IN buffer ib (n == 0: end of the stream)
   SBlock q[4];           // service warp: generated blocks, ring by block number
-  double red[2][kSCW];   // per-warp r^2 of block b in red[b & 1]
-  int nf[2][kSCW];       // per-warp non-finite flag
+  double red[2][kSCWMax];  // per-warp r^2 of block b in red[b & 1]
+  int nf[2][kSCWMax];      // per-warp non-finite flag
   PDZ_P(long long t_issue[2];)  // profiling: clock64 of IN(ib)'s TMA issue
 };
 
-// The service warp (warp kSCW) runs the CTA's whole schedule, so the compute
+// The service warp (the last warp) runs the CTA's whole schedule, so the compute
 // warps only wait for data, compute and report:
 //  * it walks the block stream (SvcIter) and posts each block's descriptor
 //    with the TMA load of its input rows into IN(b & 1), once the pass is
@@ -502,7 +518,7 @@ struct Mailbox {
 //  * with the stop rule it mirrors `fin` for the iterator.
 // Every gpu-scope fence of the CTA is executed here, one per round for all
 // purposes (release of the progress, acquire of neighbours / fin).
-template <int R, bool STOP>
+template <int R, int V, bool STOP>
 __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float* in1,
                              uint64_t* bars, const DepSet& dep, int L0, int L1) {
   const int lane = threadIdx.x & 31;
@@ -561,8 +577,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       const SBlock& b = q[dn & 3];
       // lane w holds warp w's value; a fixed butterfly sums them (lane 0's
       // result is the one stored: deterministic)
-      const double s = warp_sum(lane < kSCW ? mb->red[dn & 1][lane] : 0.0);
-      const int f = __any_sync(0xffffffffu, lane < kSCW && mb->nf[dn & 1][lane] != 0);
+      const double s = warp_sum(lane < geo_scw(V) ? mb->red[dn & 1][lane] : 0.0);
+      const int f = __any_sync(0xffffffffu, lane < geo_scw(V) && mb->nf[dn & 1][lane] != 0);
       if (acc_p != b.p || acc_it != b.iter) {
         flush();
         acc_p = b.p;
@@ -659,7 +675,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         if (lane == 0) {
           mb->desc[iss & 1] = b;
           fence_proxy_async_global();  // acquired data -> TMA (async proxy) reads
-          issue_block<R>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
+          issue_block<R, V>(a, b, (iss & 1) ? in1 : in0, &bars[iss & 1]);
           PDZ_P(mb->t_issue[iss & 1] = clock64(); PDZ_TL(a, 1, blockIdx.x, kpass);)
         }
         PDZ_P(t_iss[iss & 3] = clock64();)
@@ -714,6 +730,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
 // has published sweep n, it reduces sweep n's r^2 partials in a fixed order
 // (bitwise reproducible), applies the stop rule (solver.py:347-358) and
 // releases fin = n; it ends when every plane has stopped.
+template <int kSThreads>
 __device__ void finalizer_cta(const StreamArgs& a) {
   if (!a.st.stop_iter) return;
   __shared__ int s_run;
@@ -785,10 +802,11 @@ __device__ void finalizer_cta(const StreamArgs& a) {
 }
 
 // ------------------------------------------------------------- kernel --
-template <int R, bool EDGE, bool STOP>  // STOP: the relative-change stop rule is armed
-__global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
+template <int R, int V, bool EDGE, bool STOP>  // STOP: the relative-change stop rule is armed
+__global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA per SM
     stream_kernel(const __grid_constant__ StreamArgs a) {
-  using Gm = SGeo<R>;
+  using Gm = SGeo<R, V>;
+  constexpr int kSCW = Gm::SCW, kComputeThreads = Gm::CT, kSplit = Gm::SPLIT;
   extern __shared__ __align__(128) float smem[];
   float* const in0 = smem;
   float* const in1 = smem + Gm::IN_FLOATS;
@@ -820,13 +838,13 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
   const int WP = W + 2 * kPadC;                          // padded iterate row
   const size_t plane_pad = size_t(H + 2 * R) * WP;       // padded iterate plane
   if (blockIdx.x == a.pt.G) {  // the extra CTA: finaliser
-    finalizer_cta(a);
+    finalizer_cta<Gm::NT>(a);
     return;
   }
   if (warp == kSCW) {
     const int L0 = int(part_start(a.pt, blockIdx.x));
     const int L1 = int(part_start(a.pt, blockIdx.x + 1));
-    service_loop<R, STOP>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R), L0, L1);
+    service_loop<R, V, STOP>(a, &mb, in0, in1, bars, dep_set(a, L0, L1, R), L0, L1);
     return;
   }
 
@@ -915,7 +933,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
       if (k < Gm::RP && xr + k < Gm::PWD)
         for (int sr = tid / SL; sr < hn; sr += kComputeThreads / SL)
           in_cur[sr * Gm::PITCH + xr + k] = in_cur[sr * Gm::PITCH + xr - 1 - k];
-      compute_bar();
+      compute_bar<kComputeThreads>();
     }
     // ---- H rows: horizontal blur of the n + 2R staged rows
     // 8 adjacent outputs per item: 8 independent FMA chains, (8 + 2R)
@@ -1004,7 +1022,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     }
     if (!got2) mbar_wait(&bars[5 + ib], par);  // the vertical pass reads every row
     PDZ_P({ const long long t = clock64(); pf[2] += t - tq; tq = t; })
-    compute_bar();
+    compute_bar<kComputeThreads>();
     PDZ_P({ const long long t = clock64(); pf[3] += t - tq; tq = t; })
     mbar_wait(&bars[2], ph_pl);
     ph_pl ^= 1;
@@ -1146,7 +1164,7 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
     }
     // every read of IN / H / Phi / lambda of the block precedes this barrier
     // (H is rewritten by the next block's horizontal pass)
-    compute_bar();
+    compute_bar<kComputeThreads>();
     PDZ_P({ const long long t = clock64(); pf[6] += t - tq; tq = t; })
     ib ^= 1;
   }
@@ -1159,35 +1177,40 @@ __global__ void __maxnreg__(96)  // 20 warps x 96 registers: one CTA per SM
 // ------------------------------------------------------------------- host --
 using StreamFn = void (*)(const StreamArgs);
 
-template <int R, bool EDGE, bool STOP>
+template <int R, int V, bool EDGE, bool STOP>
 static StreamFn stream_prepared(size_t* smem) {
-  static_assert(SGeo<R>::FITS, "staging buffers exceed shared memory");
+  static_assert(SGeo<R, V>::FITS, "staging buffers exceed shared memory");
+  static_assert(SGeo<R, V>::ROWS > SGeo<R, V>::SPLIT, "two-part row load");
   static bool done = false;
-  *smem = SGeo<R>::SMEM;
+  *smem = SGeo<R, V>::SMEM;
   if (!done) {
-    cudaFuncSetAttribute(stream_kernel<R, EDGE, STOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(SGeo<R>::SMEM));
+    cudaFuncSetAttribute(stream_kernel<R, V, EDGE, STOP>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(SGeo<R, V>::SMEM));
     done = true;
   }
-  return stream_kernel<R, EDGE, STOP>;
+  return stream_kernel<R, V, EDGE, STOP>;
 }
 
-template <bool EDGE, bool STOP>
-static StreamFn stream_pick_stop(int R, size_t* smem) {
-  switch (R) {  // radii whose staging fits in shared memory (SGeo<R>::FITS)
-    case 1: return stream_prepared<1, EDGE, STOP>(smem);
-    case 2: return stream_prepared<2, EDGE, STOP>(smem);
-    case 3: return stream_prepared<3, EDGE, STOP>(smem);
-    case 6: return stream_prepared<6, EDGE, STOP>(smem);
-    case 9: return stream_prepared<9, EDGE, STOP>(smem);
-    case 12: return stream_prepared<12, EDGE, STOP>(smem);
-    case 24: return stream_prepared<24, EDGE, STOP>(smem);
+template <int V, bool EDGE, bool STOP>
+static StreamFn stream_pick_radius(int R, size_t* smem) {
+  switch (R) {  // radii whose staging fits in shared memory (SGeo<R, V>::FITS)
+    case 1: return stream_prepared<1, V, EDGE, STOP>(smem);
+    case 2: return stream_prepared<2, V, EDGE, STOP>(smem);
+    case 3: return stream_prepared<3, V, EDGE, STOP>(smem);
+    case 6: return stream_prepared<6, V, EDGE, STOP>(smem);
+    case 9: return stream_prepared<9, V, EDGE, STOP>(smem);
+    case 12: return stream_prepared<12, V, EDGE, STOP>(smem);
+    case 24: return V == 0 ? stream_prepared<24, 0, EDGE, STOP>(smem) : nullptr;
     default: return nullptr;
   }
 }
 template <bool EDGE>
-static StreamFn stream_pick(int R, bool stop, size_t* smem) {
-  return stop ? stream_pick_stop<EDGE, true>(R, smem) : stream_pick_stop<EDGE, false>(R, smem);
+static StreamFn stream_pick(int R, int V, bool stop, size_t* smem) {
+  if (V == 0)
+    return stop ? stream_pick_radius<0, EDGE, true>(R, smem)
+                : stream_pick_radius<0, EDGE, false>(R, smem);
+  return stop ? stream_pick_radius<1, EDGE, true>(R, smem)
+              : stream_pick_radius<1, EDGE, false>(R, smem);
 }
 
 }  // namespace pdz

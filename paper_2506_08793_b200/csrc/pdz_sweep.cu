@@ -341,6 +341,7 @@ struct Plan {
   int nbmax = 0;                            // partial slots per plane
   int pad_r = 0, pad_c = 0;                 // iterate buffer pads (rows, columns)
   int ring = 2;                             // iteration slots of the partials
+  int geo = 0;                              // block geometry V (pdz_stream.cuh)
   size_t smem = 0;
   void* fn = nullptr;
 };
@@ -381,11 +382,12 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
   if (allow_stream && !g_force_tiled && p->width % 4 == 0 && p->height >= 2 * P.R &&
       p->width >= 2 * rp &&
       strip_rows + p->height < (int64_t(1) << 31))
-    sfn = edge ? stream_pick<true>(P.R, p->rel_tol >= 0.0, &smem)
-               : stream_pick<false>(P.R, p->rel_tol >= 0.0, &smem);
+    sfn = edge ? stream_pick<true>(P.R, 0, p->rel_tol >= 0.0, &smem)
+               : stream_pick<false>(P.R, 0, p->rel_tol >= 0.0, &smem);
   int occ = 0;
   if (sfn) {
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, kSThreads, smem);
+    const cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sfn, geo_threads(0), smem);
     if (getenv("PDZ_VERBOSE")) {
       cudaFuncAttributes fa = {};
       cudaFuncGetAttributes(&fa, sfn);
@@ -440,6 +442,28 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
       nb = std::max<int>(nb, int(hi - lo + 1));
     }
     P.nbmax = nb;
+    // Block geometry: when a CTA's rows of a strip take several 114-row
+    // blocks per pass (configs 3 and 4), the taller 120-row / 128-register
+    // geometry needs fewer blocks per strip and runs the vertical pass with
+    // more registers; a CTA whose rows fit one block (config 2) keeps V = 0.
+    const int64_t seg_rows = P.kps > 0 ? (p->height + P.kps - 1) / P.kps : p->height;
+    P.geo = 0;
+    const char* eg = getenv("PDZ_STREAM_GEO");  // tuning / tests: force a geometry
+    const int want = eg ? atoi(eg) : (seg_rows > geo_srb(P.R, 0) ? 1 : 0);
+    if (want == 1) {
+      size_t smem1 = 0;
+      StreamFn f1 = edge ? stream_pick<true>(P.R, 1, p->rel_tol >= 0.0, &smem1)
+                         : stream_pick<false>(P.R, 1, p->rel_tol >= 0.0, &smem1);
+      int occ1 = 0;
+      if (f1 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, f1, geo_threads(1), smem1) ==
+                    cudaSuccess &&
+          occ1 >= occ) {
+        P.geo = 1;
+        P.fn = reinterpret_cast<void*>(f1);
+        P.smem = smem1;
+      }
+      cudaGetLastError();
+    }
   } else {
     cudaGetLastError();  // clear a failed occupancy query
     P.stream = false;
@@ -485,16 +509,17 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
   const int R = pl.R;
-  const int pitch = kSTW + 2 * ((R + 3) & ~3) + 4;  // = SGeo<R>::PITCH
+  const int pitch = kSTW + 2 * ((R + 3) & ~3) + 4;  // = SGeo<R, V>::PITCH
+  const int split = geo_split(pl.geo), srb = geo_srb(R, pl.geo);
   const cuuint64_t wp = cuuint64_t(p->width) + 2 * pl.pad_c;
   const cuuint64_t hp = cuuint64_t(p->height) + 2 * pl.pad_r;
   const cuuint64_t dims[3] = {wp, hp, cuuint64_t(p->planes)};
   const cuuint64_t strides[2] = {wp * 4, wp * hp * 4};
   const cuuint32_t estr[3] = {1, 1, 1};
   for (int bi = 0; bi < kNBuf; ++bi) {
-    // two boxes per block: rows [0, kSplit) and [kSplit, 2R + SRB)
-    const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(kSplit), 1};
-    const cuuint32_t box2[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + stream_srb(R) - kSplit), 1};
+    // two boxes per block: rows [0, split) and [split, 2R + SRB)
+    const cuuint32_t box[3] = {cuuint32_t(pitch), cuuint32_t(split), 1};
+    const cuuint32_t box2[3] = {cuuint32_t(pitch), cuuint32_t(2 * R + srb - split), 1};
     CUresult r = encode(&b->tm[bi], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, bufs[bi], dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -513,7 +538,7 @@ static int32_t encode_stream_maps(const pdz_solve_params* p, const Plan& pl,
       {cuuint64_t(p->width), cuuint64_t(p->height), cuuint64_t(p->planes / p->channels)}};
   const cuuint64_t dstrides[2] = {cuuint64_t(p->width) * 4,
                                   cuuint64_t(p->width) * p->height * 4};
-  const cuuint32_t dbox[3] = {cuuint32_t(kSTW), cuuint32_t(stream_srb(R)), 1};
+  const cuuint32_t dbox[3] = {cuuint32_t(kSTW), cuuint32_t(srb), 1};
   const float* dsrc[2] = {phi, lam};
   CUtensorMap* dmap[2] = {&b->tm_phi, &b->tm_lam};
   for (int k = 0; k < 2; ++k) {
@@ -615,7 +640,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.eps = float(p->epsilon);
   b.tau = float(p->tau);
   b.rel_tol = p->rel_tol;
-  b.srb = stream_srb(pl.R);
+  b.srb = geo_srb(pl.R, pl.geo);
   memcpy(b.w, w, sizeof(w));
   for (int i = 0; i < kMaxTaps; ++i) b.w2[i] = make_float2(w[i], w[i]);
   for (int i = 0; i <= kMaxTaps; ++i)
@@ -649,7 +674,7 @@ static int32_t launch_stream(const LaunchArgs& la, const Plan& pl, cudaStream_t 
   cfg.stream = s;
   cfg.dynamicSmemBytes = pl.smem;
   cfg.gridDim = dim3(pl.G + 1);  // + the finaliser CTA
-  cfg.blockDim = dim3(kSThreads);
+  cfg.blockDim = dim3(geo_threads(pl.geo));
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;

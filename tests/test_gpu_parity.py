@@ -449,3 +449,29 @@ def test_device_tensor_path(pdz):
                           ablation=("no-multiscale", "no-guided"))
     assert o_t.is_cuda
     np.testing.assert_array_equal(o_t.cpu().numpy(), o_np)
+
+
+@pytest.mark.parametrize("shape,k,edge", [((400, 136), 19, True), ((333, 128), 13, True),
+                                          ((290, 200), 25, False), ((260, 64), 7, True)])
+def test_block_geometries_agree(pdz, monkeypatch, shape, k, edge):
+    # PDZ_STREAM_K=1: one CTA per strip, so every CTA walks several blocks per
+    # pass; both block geometries (19 x 6 rows at 96 registers, 15 x 8 rows at
+    # 128) must match the oracle and each other (the same per-pixel formulas;
+    # the compiler may contract a scalar face flux differently: <= a few ulp)
+    rng = np.random.default_rng(k + shape[0])
+    ch = rng.random(shape) * 0.8 + 0.1
+    t = 0.3 + 0.6 * rng.random(shape)
+    cfg = pdz.SolverConfig(tau=TAU_STABLE if edge else 0.05, kernel_size=k,
+                           sigma=max(1.0, k / 6.0), max_iters=15, rel_tol=1e-300)
+    monkeypatch.setenv("PDZ_STREAM_K", "1")
+    us = []
+    for geo in ("0", "1"):
+        monkeypatch.setenv("PDZ_STREAM_GEO", geo)
+        u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg, edge_preserving=edge)
+        us.append((u, tr))
+    np.testing.assert_allclose(us[0][0], us[1][0], rtol=0, atol=1e-6)
+    ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg),
+                                edge_preserving=edge, separable=True)
+    for u, tr in us:
+        assert np.max(np.abs(u - ru)) <= U_TOL
+        np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
