@@ -347,6 +347,37 @@ struct Plan {
 };
 
 static int g_force_tiled = -1;
+
+// Critical-path cost of a persistent partition: every CTA runs each pass over
+// its strip segments in blocks of `srb` rows (srb1: the taller geometry, used
+// when a segment needs several blocks; 0 = unavailable), each block staging
+// 2R halo rows; the slowest CTA sets the sweep time.  Returns the largest
+// per-CTA cost in staged rows and the longest segment.
+static void partition_cost(const Partials& q, int R, int srb0, int srb1, int64_t* cost,
+                           int64_t* max_seg) {
+  int64_t worst = 0, mseg = 0;
+  for (int64_t i = 0; i < q.G; ++i) {
+    const int64_t L0 = part_start(q, i), L1 = part_start(q, i + 1);
+    for (int64_t L = L0; L < L1;) {
+      const int64_t e = std::min<int64_t>(L1, (L / q.H + 1) * q.H);
+      mseg = std::max(mseg, e - L);
+      L = e;
+    }
+  }
+  const int64_t srb = (mseg > srb0 && srb1 > 0) ? srb1 : srb0;
+  for (int64_t i = 0; i < q.G; ++i) {
+    const int64_t L0 = part_start(q, i), L1 = part_start(q, i + 1);
+    int64_t c = 0;
+    for (int64_t L = L0; L < L1;) {
+      const int64_t e = std::min<int64_t>(L1, (L / q.H + 1) * q.H);
+      c += (e - L) + 2 * R * ((e - L + srb - 1) / srb);
+      L = e;
+    }
+    worst = std::max(worst, c);
+  }
+  *cost = worst;
+  *max_seg = mseg;
+}
 #ifdef PDZ_PROFILE
 static long long* g_prof = nullptr;  // tools/prof_stream.py
 #endif  // PDZ_FORCE_TILED=1 -> always the tiled kernel
@@ -435,6 +466,29 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
     Partials q = {};
     q.S = P.S, q.U = P.U, q.G = P.G, q.kps = P.kps, q.bonus = P.bonus, q.nstr = P.nstrips;
     q.H = p->height;
+    // A per-strip partition with an integer number of CTAs per strip can
+    // leave SMs idle (configs 4 and 5: 122 of 148).  When CTAs walk several
+    // blocks per pass anyway, the even split of all strip-rows over every SM
+    // (ranges crossing strip boundaries) may be cheaper despite the extra
+    // segment halos: take whichever has the lower critical-path cost.
+    const int srb0 = geo_srb(P.R, 0);
+    const int srb1 = P.R <= 12 ? geo_srb(P.R, 1) : 0;
+    int64_t cost = 0, max_seg = 0;
+    partition_cost(q, P.R, srb0, srb1, &cost, &max_seg);
+    if (P.kps > 0 && P.S / gmax >= 2 * srb0 && !getenv("PDZ_STREAM_K")) {
+      Partials f = q;
+      f.kps = f.bonus = 0;
+      f.G = int(gmax);
+      int64_t cf = 0, mf = 0;
+      partition_cost(f, P.R, srb0, srb1, &cf, &mf);
+      if (cf < cost) {
+        q = f;
+        P.kps = P.bonus = 0;
+        P.G = f.G;
+        cost = cf;
+        max_seg = mf;
+      }
+    }
     int nb = 1;
     for (int64_t i = 0; i < images; ++i) {
       const int64_t lo = part_cta_of(q, i * P.U);
@@ -446,10 +500,9 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
     // blocks per pass (configs 3 and 4), the taller 120-row / 128-register
     // geometry needs fewer blocks per strip and runs the vertical pass with
     // more registers; a CTA whose rows fit one block (config 2) keeps V = 0.
-    const int64_t seg_rows = P.kps > 0 ? (p->height + P.kps - 1) / P.kps : p->height;
     P.geo = 0;
     const char* eg = getenv("PDZ_STREAM_GEO");  // tuning / tests: force a geometry
-    const int want = eg ? atoi(eg) : (seg_rows > geo_srb(P.R, 0) ? 1 : 0);
+    const int want = eg ? atoi(eg) : (max_seg > srb0 ? 1 : 0);
     if (want == 1) {
       size_t smem1 = 0;
       StreamFn f1 = edge ? stream_pick<true>(P.R, 1, p->rel_tol >= 0.0, &smem1)
@@ -464,6 +517,9 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
       }
       cudaGetLastError();
     }
+    if (getenv("PDZ_VERBOSE"))
+      fprintf(stderr, "pdz: plan G=%d kps=%d bonus=%d geometry=%d cost=%lld max_segment=%lld\n",
+              P.G, P.kps, P.bonus, P.geo, (long long)cost, (long long)max_seg);
   } else {
     cudaGetLastError();  // clear a failed occupancy query
     P.stream = false;

@@ -475,3 +475,20 @@ def test_block_geometries_agree(pdz, monkeypatch, shape, k, edge):
     for u, tr in us:
         assert np.max(np.abs(u - ru)) <= U_TOL
         np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
+
+
+@pytest.mark.parametrize("shape,k", [((600, 3840), 25), ((300, 7680), 49), ((600, 3000), 13)])
+def test_flat_partition_large_single_image(pdz, shape, k):
+    # tall single images: each CTA walks several blocks per pass, so the plan
+    # splits all strip-rows evenly over the SMs (ranges crossing strip
+    # boundaries: configs 4 and 5 run with it); W = 3000 adds a partial last
+    # strip
+    rng = np.random.default_rng(shape[0] + k)
+    ch = rng.random(shape) * 0.8 + 0.1
+    t = 0.3 + 0.6 * rng.random(shape)
+    cfg = pdz.SolverConfig(tau=TAU_STABLE, kernel_size=k, sigma=k / 6.0, max_iters=3,
+                           rel_tol=1e-300)
+    u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg)
+    ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg), separable=True)
+    assert np.max(np.abs(u - ru)) <= U_TOL
+    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
