@@ -475,7 +475,7 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
     const int srb1 = P.R <= 12 ? geo_srb(P.R, 1) : 0;
     int64_t cost = 0, max_seg = 0;
     partition_cost(q, P.R, srb0, srb1, &cost, &max_seg);
-    if (P.kps > 0 && P.S / gmax >= 2 * srb0 && !getenv("PDZ_STREAM_K")) {
+    if ((P.kps > 0 ? P.S / gmax >= 2 * srb0 : P.G < gmax) && !getenv("PDZ_STREAM_K")) {
       Partials f = q;
       f.kps = f.bonus = 0;
       f.G = int(gmax);
