@@ -223,6 +223,26 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
 int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float* phi,
                                      const float* lambda_map, void* workspace,
                                      size_t workspace_bytes, void* stream);
+/* A block of a row-slab solve (multi-GPU row-slab mode with k sweeps per
+ * halo exchange; paper_2506_08793_b200/parallel.py): exactly
+ * params->max_iters sweeps (rel_tol ignored) of the float32 field u_init
+ * (device [P][H][W], H = params->height: the rank's rows plus up to k*R
+ * neighbour rows above and below) instead of u0 = Phi, rows 0 and H-1
+ * treated as image borders (np.gradient ends, symmetric reflection).  Rows
+ * further than n*R from a non-border edge are exact after n sweeps, which is
+ * why the caller exchanges k*R rows every k sweeps.  Device outputs: u_out
+ * [P][H][W] the final iterate; sumsq[(n-1)*P + p] = sum of r^2 of sweep n
+ * over rows [count_lo, count_hi) (the caller all-reduces, takes the square
+ * root and applies the stop rule, solver.py:301,347-358); failed[p] = the
+ * first sweep whose counted values went non-finite, 0 if none.
+ * Asynchronous.  Workspace: pdz_solve_workspace_bytes(params).
+ * Replaces the per-sweep loop of fixed_point_solve (solver.py:343-358) for a
+ * slab. */
+int32_t pdz_fixed_point_sweeps_from(const pdz_solve_params* params, const float* u_init,
+                                    const float* phi, const float* lambda_map, int32_t count_lo,
+                                    int32_t count_hi, float* u_out, double* sumsq,
+                                    int32_t* failed, void* workspace, size_t workspace_bytes,
+                                    void* stream);
 /* Number of kernels pdz_fixed_point_sweeps_async launches for `params`
  * (benchmark bookkeeping). */
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);

@@ -17,6 +17,7 @@ struct StateView {
   int32_t* iters;       // [P] iterations whose norm is recorded
   double* prev_norm;    // [P]
   double* norms;        // [max_iters][P]
+  double* sums;         // [max_iters][P] raw sums of r^2 (nullable; row-slab blocks all-reduce them)
   int32_t* running;     // [1] planes still running after the latest finalize
   int32_t* iter_base;   // [1] first iteration of the current graph chunk
   int32_t* chunk_ctr;   // [1]
@@ -105,6 +106,7 @@ __device__ __forceinline__ int finalize_plane(const StateView& st, int P, int p,
   }
   const double norm = sqrt(s);
   st.norms[size_t(it - 1) * P + p] = norm;
+  if (st.sums) st.sums[size_t(it - 1) * P + p] = s;
   st.iters[p] = it;
   const double prev = st.prev_norm[p];
   int run = 0;

@@ -127,6 +127,7 @@ struct StreamArgs {
   int32_t iter_last, max_iters;  // sweeps 1..iter_last
   int32_t srb;          // output rows per block (geo_srb(R, V))
   int32_t stop_rule;    // rel_tol active: pass (n, c) needs fin >= n - 2
+  int32_t cnt_lo, cnt_hi;  // rows whose r^2 / non-finite flags are counted (0, H: all)
   float eps, tau;
   double rel_tol;
   long long* prof;      // -DPDZ_PROFILE builds + PDZ_PROF=1: [2G+1][16] wait times
@@ -1064,6 +1065,9 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
       const bool edge_col = lbord || wl <= kSTW;
       const bool pcl = gx == 0, pcr = gx + 1 == W - 1;
       const int nrows = col_ok ? min(kRPW, cur.n - j0) : 0;
+      // counted rows [jc0, jc1) of the warp's (row-slab blocks count only the
+      // rank's own rows, pdz_fixed_point_sweeps_from)
+      const int jc0 = a.cnt_lo - y0, jc1 = min(nrows, a.cnt_hi - y0);
       float* orow = uout + ptrdiff_t(y0) * WP + gx;
       const float* pl_row = sphi + j0 * kSTW + c;  // Phi / lambda tiles: row pitch 64
       const float* lm_row = slam + j0 * kSTW + c;
@@ -1129,8 +1133,8 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
           const float2 rr = add2(ffma2(make_float2(-lmv.x, -lmv.y), G2[j], div), phv);
           const float2 nn = ffma2(tau2, rr, cB_old);
           const float r0 = rr.x, r1 = rr.y, n0 = nn.x, n1 = nn.y;
-          if (j < nrows) {
-            *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
+          if (j < nrows) *reinterpret_cast<float2*>(orow) = make_float2(n0, n1);
+          if (j >= jc0 && j < jc1) {
             r2p = ffma2(rr, rr, r2p);
             nfp = ffma2(nn, zero2, nfp);  // NaN iff non-finite update
           }

@@ -53,6 +53,7 @@ struct SweepArgs {
   // global row y + y_off of an H_glob-row image; only rows [row_lo, row_hi)
   // are written and counted in the norms.  Whole image: 0, H, 0, H.
   int32_t y_off, H_glob, row_lo, row_hi;
+  int32_t cnt_lo, cnt_hi;  // rows counted in the norms (within the row window)
   float eps, tau;
   double rel_tol;
   float w[kMaxTaps];     // 1-D Gaussian taps (kernel params -> constant bank)
@@ -218,8 +219,10 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const SweepArgs a) {
       const float r = fmaf(-lam[off], G[j], div) + phi[off];
       const float un = fmaf(a.tau, r, U[j + 1][1]);
       uout[off] = un;
-      acc2 = fma(double(r), double(r), acc2);
-      nf |= !(isfinite(r) && isfinite(un));
+      if (gy >= a.cnt_lo && gy < a.cnt_hi) {
+        acc2 = fma(double(r), double(r), acc2);
+        nf |= !(isfinite(r) && isfinite(un));
+      }
     }
   }
 
@@ -661,6 +664,8 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   a.H_glob = p->height;
   a.row_lo = 0;
   a.row_hi = p->height;
+  a.cnt_lo = 0;
+  a.cnt_hi = p->height;
   memcpy(a.w, w, sizeof(w));
   StreamArgs& b = la->stream;
   b.buf[0] = buf0;
@@ -681,6 +686,8 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.iter_last = p->max_iters;
   b.max_iters = p->max_iters;
   b.stop_rule = (p->rel_tol >= 0.0) ? 1 : 0;
+  b.cnt_lo = 0;
+  b.cnt_hi = p->height;
 #ifdef PDZ_PROFILE
   if (const char* e = getenv("PDZ_PROF")) {
     if (e[0] == '1' && pl.stream) {
@@ -823,6 +830,7 @@ static SolveLayout carve_solve(const pdz_solve_params* p, const Plan& pl, void* 
   L.st.iters = c.take<int32_t>(P);
   L.st.prev_norm = c.take<double>(P);
   L.st.norms = c.take<double>(size_t(p->max_iters) * P);
+  L.st.sums = c.take<double>(size_t(p->max_iters) * P);
   L.st.running = c.take<int32_t>(1);
   L.st.iter_base = c.take<int32_t>(1);
   L.st.chunk_ctr = c.take<int32_t>(1);
@@ -913,17 +921,24 @@ static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const So
   return PDZ_OK;
 }
 
+// u_init: the first iterate (nullptr: u0 = Phi, solver.py:333); rows
+// [cnt_lo, cnt_hi) are the ones counted in the norms.
 static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
                            const float* phi, const float* lam, float* out, cudaStream_t s,
-                           bool poll) {
+                           bool poll, const float* u_init = nullptr, int cnt_lo = 0,
+                           int cnt_hi = -1) {
   LaunchArgs la;
   int32_t rc = fill_args(p, pl, L.buf0, L.buf1, L.buf2, phi, lam, L.psum, L.pflag, L.st, L.sy,
                          &la);
   if (rc != PDZ_OK) return rc;
+  if (cnt_hi < 0) cnt_hi = p->height;
+  la.tile.cnt_lo = la.stream.cnt_lo = cnt_lo;
+  la.tile.cnt_hi = la.stream.cnt_hi = cnt_hi;
+  if (u_init == nullptr) u_init = phi;
   {
     const int64_t n = int64_t(p->planes) * (p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
     const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
-    pad_init_kernel<<<blocks, 256, 0, s>>>(phi, L.buf0, pl.stream ? L.buf1 : nullptr, L.buf2,
+    pad_init_kernel<<<blocks, 256, 0, s>>>(u_init, L.buf0, pl.stream ? L.buf1 : nullptr, L.buf2,
                                            p->height, p->width, p->planes, pl.pad_r, pl.pad_c);
     PDZ_CHECK_LAUNCH("u0 = Phi");
   }
@@ -1052,8 +1067,8 @@ static int32_t step_impl(const pdz_solve_params* params, const float* u, float* 
   if (rc != PDZ_OK) return rc;
   la.tile.y_off = y_off;
   la.tile.H_glob = H_glob;
-  la.tile.row_lo = row_lo;
-  la.tile.row_hi = row_hi;
+  la.tile.row_lo = la.tile.cnt_lo = row_lo;
+  la.tile.row_hi = la.tile.cnt_hi = row_hi;
   cudaStream_t s = as_stream(stream);
   rc = launch_tiled(la, &one, pl, 1, s, false);
   if (rc != PDZ_OK) return rc;
@@ -1162,6 +1177,37 @@ int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float
     return PDZ_EWORKSPACE;
   }
   return queue_solve(&fixed, pl, L, phi, lambda_map, L.out, as_stream(stream), false);
+}
+
+int32_t pdz_fixed_point_sweeps_from(const pdz_solve_params* params, const float* u_init,
+                                    const float* phi, const float* lambda_map, int32_t count_lo,
+                                    int32_t count_hi, float* u_out, double* sumsq,
+                                    int32_t* failed, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+  Plan pl;
+  int32_t rc = solve_plan(params, phi, lambda_map, &pl);
+  if (rc != PDZ_OK) return rc;
+  PDZ_REQUIRE(u_init && phi && lambda_map && u_out && sumsq && failed, "NULL array argument");
+  PDZ_REQUIRE(u_init != u_out, "u_out must not alias u_init");
+  PDZ_REQUIRE(0 <= count_lo && count_lo < count_hi && count_hi <= params->height,
+              "count window [%d, %d) outside the %d rows", count_lo, count_hi, params->height);
+  pdz_solve_params fixed = *params;
+  fixed.rel_tol = -1.0;  // exactly max_iters sweeps: the caller applies the stop rule
+  SolveLayout L = carve_solve(&fixed, pl, workspace, workspace_bytes);
+  if (workspace == nullptr || L.bytes > workspace_bytes) {
+    set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
+    return PDZ_EWORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  rc = queue_solve(&fixed, pl, L, phi, lambda_map, u_out, s, false, u_init, count_lo, count_hi);
+  if (rc != PDZ_OK) return rc;
+  const size_t P = params->planes;
+  PDZ_CUDA(cudaMemcpyAsync(sumsq, L.st.sums, size_t(params->max_iters) * P * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s),
+           "sums copy");
+  PDZ_CUDA(cudaMemcpyAsync(failed, L.st.failed, P * sizeof(int32_t), cudaMemcpyDeviceToDevice, s),
+           "failed copy");
+  return PDZ_OK;
 }
 
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {

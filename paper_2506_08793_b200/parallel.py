@@ -8,24 +8,30 @@ Row-slab mode (configs 4 and 5, one large image) is implemented here:
 * every rank runs the (cheap, < 1 %) front end on the whole image, so all
   ranks hold identical Phi, lambda and tau bounds;
 * rank k owns the global rows [y0, y1) = slab_bounds(H, G, k) of ALL C
-  planes, stored as an extended slab of R + (y1 - y0) + R rows,
-  R = max(1, K // 2);
-* before every sweep the R halo rows are exchanged with the neighbouring
-  ranks (torch.distributed point-to-point: NCCL on GPUs, gloo in the CPU
-  tests); at the global top / bottom the halo is the symmetric reflection of
-  the slab's own rows (np.pad "symmetric", solver.py:235);
-* one sweep of the slab runs on the device through
-  pdz_fixed_point_step_rows (include/pdz.h), which knows the global row of
-  every array row -- np.gradient's one-sided rows (solver.py:178-179) exist
-  only at the global border, and the reflected halo makes the zero-flux
-  border (solver.py:205-209) exact;
-* the per-plane sums of r^2 are all-reduced every sweep, so every rank
-  applies the same global stop rule (solver.py:347-358);
+  planes;
+* the solve advances in BLOCKS of k sweeps (temporal blocking): before a
+  block the ranks exchange k*R rows with each neighbour (torch.distributed
+  point-to-point: NCCL on GPUs, gloo in the CPU tests), R = max(1, K // 2),
+  so each rank holds an extended slab of its rows plus up to k*R neighbour
+  rows on each side.  One sweep moves information R rows, so after n <= k
+  sweeps of the extended slab treated as an image of its own (rows 0 / E-1
+  as image borders: exactly the global borders at the top of rank 0 and the
+  bottom of rank G-1, fake ones elsewhere) the rank's own rows are exact --
+  bit for bit the whole-image arithmetic;
+* a block runs on the device as ONE persistent-kernel launch
+  (pdz_fixed_point_sweeps_from, include/pdz.h): k sweeps starting from the
+  current iterate, counting r^2 only over the rank's own rows;
+* the [k][C] table of per-sweep sums of r^2 is all-reduced once per block,
+  and every rank applies the same global stop rule (solver.py:347-358) to
+  the k sweeps in order; a plane that stopped inside a block takes the
+  iterate after its stopping sweep, recomputed from the block's start;
 * the final slabs are all-gathered into the full image on every rank.
 
-The sweep itself is pluggable (`step=`) so the CPU tests can drive the same
-host logic with an oracle step on CPU tensors; the default step is the CUDA
-one and there is no CPU fallback in the product.
+k trades the redundant halo sweeps (2kR rows per block) against one
+exchange + all-reduce + launch per block; the default is
+min(8, slab rows // R).  The block engine is pluggable (`block=`) so the CPU
+tests drive the same host logic with an oracle engine on CPU tensors; the
+default engine is the CUDA one and there is no CPU fallback in the product.
 """
 
 from __future__ import annotations
@@ -39,7 +45,8 @@ from .image import to_host, validate_image
 
 logger = logging.getLogger("pdehaze.solver")
 
-__all__ = ["slab_bounds", "halo_rows", "SlabSolver", "solve_slab", "dehaze_slabs"]
+__all__ = ["slab_bounds", "halo_rows", "default_sweeps_per_exchange", "SlabSolver",
+           "solve_slab", "dehaze_slabs"]
 
 
 def slab_bounds(height: int, world: int, rank: int) -> tuple[int, int]:
@@ -64,149 +71,175 @@ def _global_rank(group, r):
     return r if group is None else dist.get_global_rank(group, r)
 
 
-def _cuda_step(cfg: SolverConfig, tau: float, edge_preserving: bool):
-    """The product sweep: pdz_fixed_point_step_rows on device tensors."""
+def _cuda_block(cfg: SolverConfig, tau: float, edge_preserving: bool):
+    """The product block engine: pdz_fixed_point_sweeps_from on device tensors
+    (one persistent launch per block)."""
     import torch
 
     lib = nat.lib()
     from .solver import _params
 
-    def step(u_in, u_out, phi_e, lam_e, y_off, height, row_lo, row_hi):
-        planes, rows, width = u_in.shape
-        prm = _params(rows, width, planes, planes, cfg, edge_preserving=edge_preserving, tau=tau)
-        ws = nat.workspace(lib.pdz_step_workspace_bytes(prm), "slab")
-        sums = torch.empty(planes, dtype=torch.float64, device=u_in.device)
-        nf = torch.empty(planes, dtype=torch.int32, device=u_in.device)
-        nat.check(lib.pdz_fixed_point_step_rows(
-            prm, nat.ptr(u_in), nat.ptr(u_out), nat.ptr(phi_e), nat.ptr(lam_e), int(y_off),
-            int(height), int(row_lo), int(row_hi), nat.ptr(sums), nat.ptr(nf), nat.ptr(ws),
-            ws.numel(), nat.stream_ptr()))
-        return sums, nf
+    def block(u_ext, phi_e, lam_e, lo, hi, n):
+        planes, rows, width = u_ext.shape
+        # lambda has one plane shared by all planes: channels = planes
+        prm = _params(rows, width, planes, planes, cfg, edge_preserving=edge_preserving,
+                      tau=tau, max_iters=n)
+        ws = nat.workspace(lib.pdz_solve_workspace_bytes(prm), "slab")
+        out = torch.empty_like(u_ext)
+        sums = torch.empty((n, planes), dtype=torch.float64, device=u_ext.device)
+        failed = torch.empty(planes, dtype=torch.int32, device=u_ext.device)
+        nat.check(lib.pdz_fixed_point_sweeps_from(
+            prm, nat.ptr(u_ext), nat.ptr(phi_e), nat.ptr(lam_e), int(lo), int(hi), nat.ptr(out),
+            nat.ptr(sums), nat.ptr(failed), nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+        return out, sums, failed
 
-    return step
+    return block
+
+
+def default_sweeps_per_exchange(min_rows: int, halo: int, world: int, max_iters: int) -> int:
+    """k of the temporal blocking: one block for a single rank; else at most
+    8 sweeps and never deeper than a neighbour's slab (k*R <= its rows)."""
+    if world == 1:
+        return max(1, max_iters)
+    return max(1, min(8, min_rows // halo, max_iters))
 
 
 class SlabSolver:
     """One rank's share of a row-slab solve.
 
     phi: (C, H, W) full Phi (every rank holds it after the replicated front
-    end) or just this rank's rows (C, y1 - y0, W) with `full=False`;
-    lam: (H, W) or (y1 - y0, W) likewise.
+    end); lam: (H, W).  `sweeps_per_exchange` = k of the temporal blocking
+    (default: default_sweeps_per_exchange).
     """
 
     def __init__(self, phi, lam, height: int, cfg: SolverConfig, *, tau: float,
                  edge_preserving: bool = True, group=None, rank: int = 0, world: int = 1,
-                 full: bool = True, step=None):
-        import torch
-
+                 block=None, sweeps_per_exchange: int | None = None):
         self.cfg, self.tau, self.height = cfg, float(tau), int(height)
         self.group, self.rank, self.world = group, rank, world
         self.y0, self.y1 = slab_bounds(self.height, world, rank)
         self.rows = self.y1 - self.y0
         self.halo = R = halo_rows(cfg.kernel_size)
-        last_rows = self.height - slab_bounds(self.height, world, world - 1)[0]
-        if last_rows < R or self.rows < R:
+        min_rows = min(slab_bounds(self.height, world, k)[1] - slab_bounds(self.height, world, k)[0]
+                       for k in range(world))
+        if min_rows < R:
             raise ValueError(f"{world} row slabs of a {self.height}-row image leave fewer than "
                              f"the {R} halo rows per slab")
-        planes, _, width = phi.shape
-        self.planes, self.width = planes, width
-        E = self.rows + 2 * R
-        kw = dict(dtype=phi.dtype, device=phi.device)
-        self.phi_e = torch.zeros((planes, E, width), **kw)
-        self.lam_e = torch.zeros((E, width), dtype=lam.dtype, device=lam.device)
-        src_phi = phi[:, self.y0:self.y1] if full else phi
-        src_lam = lam[self.y0:self.y1] if full else lam
-        self.phi_e[:, R:R + self.rows] = src_phi
-        self.lam_e[R:R + self.rows] = src_lam
-        self.u = [self.phi_e.clone(), torch.zeros_like(self.phi_e)]  # u0 = Phi (solver.py:333)
-        self.step = step or _cuda_step(cfg, self.tau, edge_preserving)
-        self._recv = [torch.empty((planes, R, width), **kw) for _ in range(2)]
+        k = sweeps_per_exchange or default_sweeps_per_exchange(min_rows, R, world, cfg.max_iters)
+        if world > 1 and k * R > min_rows:
+            raise ValueError(f"{k} sweeps per exchange need {k * R} halo rows, more than the "
+                             f"{min_rows} rows of the thinnest slab")
+        self.k = int(k)
+        depth = self.k * R if world > 1 else 0
+        self.top = min(depth, self.y0)                  # neighbour rows above
+        self.bot = min(depth, self.height - self.y1)    # and below
+        a, b = self.y0 - self.top, self.y1 + self.bot   # global rows of the extended slab
+        self.planes, self.width = phi.shape[0], phi.shape[2]
+        self.phi_e = phi[:, a:b].contiguous().clone()
+        self.lam_e = lam[a:b].contiguous().clone()
+        self.u = self.phi_e.clone()  # u0 = Phi (solver.py:333)
+        self.block = block or _cuda_block(cfg, self.tau, edge_preserving)
 
     # -- halo exchange -----------------------------------------------------
     def exchange(self, u):
-        """Fill the R halo rows above and below the slab of `u` (C, E, W)."""
+        """Fill the neighbour rows of the extended slab `u` (C, E, W) with the
+        neighbours' current rows."""
+        if self.world == 1 or (self.top == 0 and self.bot == 0):
+            return
         import torch
+        import torch.distributed as dist
 
-        R, n = self.halo, self.rows
-        ops = []
-        if self.world > 1:
-            import torch.distributed as dist
-
-            if self.rank > 0:
-                peer = _global_rank(self.group, self.rank - 1)
-                ops.append(dist.P2POp(dist.isend, u[:, R:2 * R].contiguous(), peer, self.group))
-                ops.append(dist.P2POp(dist.irecv, self._recv[0], peer, self.group))
-            if self.rank < self.world - 1:
-                peer = _global_rank(self.group, self.rank + 1)
-                ops.append(dist.P2POp(dist.isend, u[:, n:n + R].contiguous(), peer, self.group))
-                ops.append(dist.P2POp(dist.irecv, self._recv[1], peer, self.group))
-            for req in dist.batch_isend_irecv(ops) if ops else []:
-                req.wait()
+        t, n = self.top, self.rows
+        ops, recv = [], {}
         if self.rank > 0:
-            u[:, :R] = self._recv[0]
-        else:  # global top: rows -1-i <- i
-            u[:, :R] = torch.flip(u[:, R:2 * R], dims=[1])
+            peer = _global_rank(self.group, self.rank - 1)
+            # the rank above holds `t` rows of ours below its slab
+            ops.append(dist.P2POp(dist.isend, u[:, t:t + t].contiguous(), peer, self.group))
+            recv["top"] = torch.empty_like(u[:, :t])
+            ops.append(dist.P2POp(dist.irecv, recv["top"], peer, self.group))
         if self.rank < self.world - 1:
-            u[:, n + R:] = self._recv[1]
-        else:  # global bottom: rows H+i <- H-1-i
-            u[:, n + R:] = torch.flip(u[:, n:n + R], dims=[1])
+            peer = _global_rank(self.group, self.rank + 1)
+            b = self.bot
+            ops.append(dist.P2POp(dist.isend, u[:, t + n - b:t + n].contiguous(), peer,
+                                  self.group))
+            recv["bot"] = torch.empty_like(u[:, t + n:])
+            ops.append(dist.P2POp(dist.irecv, recv["bot"], peer, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if "top" in recv:
+            u[:, :t] = recv["top"]
+        if "bot" in recv:
+            u[:, t + n:] = recv["bot"]
 
-    def _allreduce(self, sums, nf):
+    def _allreduce(self, sums, failed):
         if self.world > 1:
+            import torch
             import torch.distributed as dist
 
             dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=self.group)
-            dist.all_reduce(nf, op=dist.ReduceOp.MAX, group=self.group)
-        return sums, nf
+            big = torch.iinfo(torch.int32).max
+            first = torch.where(failed > 0, failed, torch.full_like(failed, big))
+            dist.all_reduce(first, op=dist.ReduceOp.MIN, group=self.group)
+            failed = torch.where(first == big, torch.zeros_like(first), first)
+        return sums, failed
 
     # -- the solve -----------------------------------------------------------
     def solve(self, max_iters: int, rel_tol: float):
         """fixed_point_solve (solver.py:343-358) of every plane over the slab.
         Returns (u slab (C, y1 - y0, W), norms [C] lists, iterations [C],
         converged [C])."""
-        R, n = self.halo, self.rows
+        t, n = self.top, self.rows
         P = self.planes
-        result = self.u[0][:, R:R + n].clone()
+        u = self.u
+        result = u[:, t:t + n].clone()
         running = [True] * P
         prev = [None] * P
         norms = [[] for _ in range(P)]
         iters = [0] * P
         conv = [False] * P
-        cur = 0
-        for it in range(1, max_iters + 1):
-            u_in, u_out = self.u[cur], self.u[cur ^ 1]
-            self.exchange(u_in)
-            sums, nf = self.step(u_in, u_out, self.phi_e, self.lam_e, self.y0 - R, self.height,
-                                 R, R + n)
-            sums, nf = self._allreduce(sums, nf)
+        it = 0
+        while it < max_iters and any(running):
+            k = min(self.k, max_iters - it)
+            self.exchange(u)
+            u_new, sums, failed = self.block(u, self.phi_e, self.lam_e, t, t + n, k)
+            sums, failed = self._allreduce(sums, failed)
             sums_h = sums.to("cpu").numpy()
-            nf_h = nf.to("cpu").numpy()
-            cur ^= 1
-            for p in range(P):
-                if not running[p]:
-                    continue
-                if nf_h[p]:
-                    raise FloatingPointError(
-                        f"solver produced non-finite values at iteration {it}")
-                nrm = math.sqrt(float(sums_h[p]))
-                norms[p].append(nrm)
-                iters[p] = it
-                stop = False
-                if prev[p] is not None and abs(nrm - prev[p]) / max(prev[p], 1e-30) <= rel_tol:
-                    conv[p] = stop = True
-                elif it >= max_iters:
-                    stop = True
-                prev[p] = nrm
-                if stop:  # the answer is the iterate after the stopping update
-                    running[p] = False
-                    result[p] = self.u[cur][p, R:R + n]
-            if not any(running):
-                break
+            failed_h = failed.to("cpu").numpy()
+            stop_at = {}
+            for s in range(1, k + 1):
+                for p in range(P):
+                    if not running[p]:
+                        continue
+                    if 0 < failed_h[p] <= s:
+                        raise FloatingPointError(
+                            f"solver produced non-finite values at iteration {it + s}")
+                    nrm = math.sqrt(float(sums_h[s - 1, p]))
+                    norms[p].append(nrm)
+                    iters[p] = it + s
+                    stop = False
+                    if prev[p] is not None and abs(nrm - prev[p]) / max(prev[p], 1e-30) <= rel_tol:
+                        conv[p] = stop = True
+                    elif it + s >= max_iters:
+                        stop = True
+                    prev[p] = nrm
+                    if stop:
+                        running[p] = False
+                        stop_at[p] = s
+            # the answer is the iterate after the stopping update: recomputed
+            # from the block's start for a plane that stopped inside the block
+            for s in sorted(set(stop_at.values())):
+                u_s = u_new if s == k else self.block(u, self.phi_e, self.lam_e, t, t + n, s)[0]
+                for p, sp in stop_at.items():
+                    if sp == s:
+                        result[p] = u_s[p, t:t + n]
+            u = u_new
+            it += k
+        self.u = u
         return result, norms, iters, conv
 
 
 def solve_slab(phi, lam, height, cfg: SolverConfig, *, tau=None, edge_preserving=True,
-               bounds=None, group=None, step=None, full=True, warn=True):
+               bounds=None, group=None, block=None, sweeps_per_exchange=None, warn=True):
     """Row-slab fixed_point_solve of all C planes on the calling rank.
     Returns (u slab (C, rows, W), [SolverTrace] * C) -- the traces (global
     norms) are identical on every rank."""
@@ -226,7 +259,8 @@ def solve_slab(phi, lam, height, cfg: SolverConfig, *, tau=None, edge_preserving
                     "relaxation step %.3g exceeds the stability bound %.3g at the "
                     "initial iterate; convergence is not guaranteed", step_size, b)
     solver = SlabSolver(phi, lam, height, cfg, tau=step_size, edge_preserving=edge_preserving,
-                        group=group, rank=rank, world=world, full=full, step=step)
+                        group=group, rank=rank, world=world, block=block,
+                        sweeps_per_exchange=sweeps_per_exchange)
     u, norms, iters, conv = solver.solve(cfg.max_iters, cfg.rel_tol)
     bl = list(bounds) if bounds is not None else [float("nan")] * solver.planes
     traces = [SolverTrace(residual_norms=norms[p], iterations_run=iters[p], converged=conv[p],

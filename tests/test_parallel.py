@@ -1,7 +1,8 @@
 """Row-slab multi-GPU host logic (paper_2506_08793_b200/parallel.py)
-on CPU: the slab driver's halo exchange, global stop rule and gather run with
-torch.distributed over gloo (world size 1 and 2), the sweep itself being the
-oracle restatement applied to the extended slab (test infrastructure).  The
+on CPU: the slab driver's halo exchange (k*R rows every k sweeps), global stop rule
+and gather run with torch.distributed over gloo (world sizes 1, 2 and 3), the
+block engine being the oracle restatement applied to the extended slab (test
+infrastructure).  The
 restored field must equal the single-process oracle solve bit for bit (every
 pixel's arithmetic is the same) and the residual norms to 1e-12 (only the
 summation split differs)."""
@@ -19,81 +20,35 @@ import torch.multiprocessing as mp
 from conftest import TAU_STABLE
 from oracle import pdz_oracle as orc
 from paper_2506_08793_b200 import SolverConfig
-from paper_2506_08793_b200.parallel import SlabSolver, halo_rows, slab_bounds, solve_slab
+from paper_2506_08793_b200.parallel import (SlabSolver, default_sweeps_per_exchange, halo_rows,
+                                             slab_bounds, solve_slab)
 
 
-# ---------------------------------------------------------------- oracle step
+# ---------------------------------------------------------------- oracle block
 
-def _gy_global(u, y_off, height):
-    """np.gradient along rows of the extended slab with the one-sided ends
-    only at global rows 0 / H-1 (there the reflected halo row equals the edge
-    row, so u[i+1] - u[i-1] is exactly np.gradient's one-sided difference)."""
-    g = np.empty_like(u)
-    g[1:-1] = (u[2:] - u[:-2]) / 2.0
-    g[0] = u[1] - u[0]
-    g[-1] = u[-1] - u[-2]
-    for i in range(1, u.shape[0] - 1):
-        if i + y_off in (0, height - 1):
-            g[i] = u[i + 1] - u[i - 1]
-    return g
-
-
-def _slab_divergence(u, eps, edge, y_off, height):
-    je = u[:, 1:] - u[:, :-1]
-    js = u[1:, :] - u[:-1, :]
-    if edge:
-        gy = _gy_global(u, y_off, height)
-        gx = orc._centred(u, 1)
-        te = 0.5 * (gy[:, 1:] + gy[:, :-1])
-        ts = 0.5 * (gx[1:, :] + gx[:-1, :])
-        de = 1.0 / (np.sqrt(je * je + te * te) + eps)
-        ds = 1.0 / (np.sqrt(js * js + ts * ts) + eps)
-    else:
-        de, ds = np.ones_like(je), np.ones_like(js)
-    fe, fs = de * je, ds * js
-    acc = np.zeros_like(u)
-    acc[:, :-1] = acc[:, :-1] + fe
-    acc[:, 1:] = acc[:, 1:] - fe
-    acc[:-1, :] = acc[:-1, :] + fs
-    acc[1:, :] = acc[1:, :] - fs
-    return acc
-
-
-def _slab_blur(u, sigma, size, lo, hi):
-    """gaussian_blur_separable restricted to rows [lo, hi) of the slab; the
-    R rows above / below come from the halo instead of reflection."""
-    h, w = u.shape
-    r = size // 2
-    g = orc.gaussian_taps_1d(sigma, size)
-    cols = orc.reflect_index(np.arange(-r, w + r), w)
-    ext = u[:, cols]
-    tmp = np.zeros_like(u)
-    for b in range(size):
-        tmp += g[b] * ext[:, b:b + w]
-    out = np.zeros((hi - lo, w))
-    for a in range(size):
-        out += g[a] * tmp[lo - r + a:hi - r + a, :]
-    return out
-
-
-def oracle_slab_step(settings, tau, edge=True):
-    def step(u_in, u_out, phi_e, lam_e, y_off, height, lo, hi):
-        u = u_in.numpy()
+def oracle_block(settings, tau, edge=True):
+    """Block engine for the CPU tests: n oracle sweeps (relaxed_step's
+    arithmetic, separable Gaussian) of the extended slab as an image of its
+    own, r^2 counted over rows [lo, hi)."""
+    def block(u_ext, phi_e, lam_e, lo, hi, n):
+        u = u_ext.numpy().copy()
         src, lam = phi_e.numpy(), lam_e.numpy()
-        out = u_out.numpy()
         planes = u.shape[0]
-        sums = np.zeros(planes)
-        nf = np.zeros(planes, dtype=np.int32)
+        sums = np.zeros((n, planes))
+        failed = np.zeros(planes, dtype=np.int32)
         for p in range(planes):
-            div = _slab_divergence(u[p], settings.epsilon, edge, y_off, height)[lo:hi]
-            r = div - lam[lo:hi] * _slab_blur(u[p], settings.sigma, settings.kernel_size,
-                                              lo, hi) + src[p, lo:hi]
-            out[p, lo:hi] = u[p, lo:hi] + tau * r
-            sums[p] = np.sum(r * r)
-            nf[p] = int(not (np.all(np.isfinite(r)) and np.all(np.isfinite(out[p, lo:hi]))))
-        return torch.from_numpy(sums), torch.from_numpy(nf)
+            for s in range(n):
+                r = (orc.flux_divergence(u[p], settings.epsilon, edge)
+                     - lam * orc.gaussian_blur_separable(u[p], settings.sigma,
+                                                         settings.kernel_size) + src[p])
+                u[p] = u[p] + tau * r
+                sums[s, p] = np.sum(r[lo:hi] * r[lo:hi])
+                if not failed[p] and not (np.all(np.isfinite(r[lo:hi]))
+                                          and np.all(np.isfinite(u[p, lo:hi]))):
+                    failed[p] = s + 1
+        return torch.from_numpy(u), torch.from_numpy(sums), torch.from_numpy(failed)
 
-    return step
+    return block
 
 
 # ------------------------------------------------------------------- inputs
@@ -137,20 +92,28 @@ def test_slab_bounds_cover_the_image():
     assert halo_rows(25) == 12 and halo_rows(49) == 24 and halo_rows(1) == 1
     with pytest.raises(ValueError):
         slab_bounds(10, 2, 2)
+    # C4 at G = 8 (270 rows, R = 12): 8 sweeps per exchange; C5 (540, 24): 8
+    assert default_sweeps_per_exchange(270, 12, 8, 500) == 8
+    assert default_sweeps_per_exchange(30, 12, 8, 500) == 2
+    assert default_sweeps_per_exchange(540, 24, 8, 3) == 3
+    assert default_sweeps_per_exchange(10, 3, 1, 200) == 200
 
 
 def test_slab_too_thin_for_the_halo():
     img, t, a, st, phi, lam = _problem(h=20)
     with pytest.raises(ValueError, match="halo"):
         SlabSolver(torch.from_numpy(phi), torch.from_numpy(lam), 20, _cfg(st), tau=st.tau,
-                   rank=0, world=8, step=oracle_slab_step(st, st.tau))
+                   rank=0, world=8, block=oracle_block(st, st.tau))
+    with pytest.raises(ValueError, match="sweeps per exchange"):
+        SlabSolver(torch.from_numpy(phi), torch.from_numpy(lam), 20, _cfg(st), tau=st.tau,
+                   rank=0, world=2, block=oracle_block(st, st.tau), sweeps_per_exchange=4)
 
 
 def test_single_slab_equals_the_oracle_bitwise():
     img, t, a, st, phi, lam = _problem()
     ref_u, ref_tr = _reference(img, t, a, st)
     u, traces = solve_slab(torch.from_numpy(phi), torch.from_numpy(lam), phi.shape[1], _cfg(st),
-                           step=oracle_slab_step(st, st.tau), warn=False)
+                           block=oracle_block(st, st.tau), warn=False)
     np.testing.assert_array_equal(u.numpy(), ref_u)
     for tr, rt in zip(traces, ref_tr):
         assert tr.residual_norms == rt.residual_norms
@@ -163,7 +126,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, outdir, max_iters, rel_tol):
+def _worker(rank, world, port, outdir, max_iters, rel_tol, k):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -171,16 +134,21 @@ def _worker(rank, world, port, outdir, max_iters, rel_tol):
         img, t, a, st, phi, lam = _problem()
         cfg = _cfg(st, max_iters, rel_tol)
         solver = SlabSolver(torch.from_numpy(phi), torch.from_numpy(lam), phi.shape[1], cfg,
-                            tau=st.tau, rank=rank, world=world, step=oracle_slab_step(st, st.tau))
-        # halo exchange: after one exchange the halos hold the neighbours' rows
-        u = solver.u[0].clone()
+                            tau=st.tau, rank=rank, world=world, block=oracle_block(st, st.tau),
+                            sweeps_per_exchange=k)
+        # halo exchange: the neighbour rows of the extended slab are replaced by
+        # the neighbours' current rows (here: a marked copy of Phi)
+        y0, y1, t, b = solver.y0, solver.y1, solver.top, solver.bot
+        assert t == (0 if rank == 0 else k * solver.halo)
+        assert b == (0 if rank == world - 1 else k * solver.halo)
+        u = solver.u.clone()
+        u[:, :t] = -1.0
+        u[:, t + solver.rows:] = -1.0
         solver.exchange(u)
-        R, n = solver.halo, solver.rows
-        y0, y1 = solver.y0, solver.y1
-        rows = orc.reflect_index(np.arange(y0 - R, y1 + R), phi.shape[1])
-        np.testing.assert_array_equal(u.numpy(), phi[:, rows])
+        np.testing.assert_array_equal(u.numpy(), phi[:, y0 - t:y1 + b])
         u_slab, traces = solve_slab(torch.from_numpy(phi), torch.from_numpy(lam), phi.shape[1],
-                                    cfg, step=oracle_slab_step(st, st.tau), warn=False)
+                                    cfg, block=oracle_block(st, st.tau), sweeps_per_exchange=k,
+                                    warn=False)
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), u=u_slab.numpy(), y0=y0, y1=y1,
                  **{f"norms{c}": np.array(tr.residual_norms) for c, tr in enumerate(traces)},
                  iters=np.array([tr.iterations_run for tr in traces]),
@@ -189,19 +157,20 @@ def _worker(rank, world, port, outdir, max_iters, rel_tol):
         dist.destroy_process_group()
 
 
-def _run_world(world, max_iters=12, rel_tol=1e-300):
+def _run_world(world, max_iters=12, rel_tol=1e-300, k=2):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), d, max_iters, rel_tol), nprocs=world,
+        mp.spawn(_worker, args=(world, _free_port(), d, max_iters, rel_tol, k), nprocs=world,
                  join=True)
         return [np.load(os.path.join(d, f"rank{k}.npz"), allow_pickle=True)
                 for k in range(world)]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_slabs_over_gloo_match_the_oracle(world):
+@pytest.mark.parametrize("world,k", [(2, 1), (2, 3), (3, 2), (3, 4)])
+def test_row_slabs_over_gloo_match_the_oracle(world, k):
+    # 12 sweeps in blocks of k (the last block shorter when k does not divide 12)
     img, t, a, st, phi, lam = _problem()
     ref_u, ref_tr = _reference(img, t, a, st)
-    parts = _run_world(world)
+    parts = _run_world(world, k=k)
     u = np.concatenate([p["u"] for p in parts], axis=1)
     np.testing.assert_array_equal(u, ref_u)
     for p in parts:  # every rank holds the same global trace
@@ -216,7 +185,9 @@ def test_row_slabs_share_the_global_stop_rule():
                                 max_iters=200, rel_tol=2e-3)
     ref_u, ref_tr = _reference(img, t, a, st_tol)
     assert all(tr.converged for tr in ref_tr) and ref_tr[0].iterations_run < 200
-    parts = _run_world(2, max_iters=200, rel_tol=2e-3)
+    # blocks of 3 sweeps: planes stop inside blocks and take the recomputed
+    # iterate after their stopping sweep
+    parts = _run_world(2, max_iters=200, rel_tol=2e-3, k=3)
     u = np.concatenate([p["u"] for p in parts], axis=1)
     for c in range(3):
         assert [int(p["iters"][c]) for p in parts] == [ref_tr[c].iterations_run] * 2
