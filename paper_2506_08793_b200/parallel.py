@@ -29,7 +29,8 @@ Row-slab mode (configs 4 and 5, one large image) is implemented here:
 
 k trades the redundant halo sweeps (2kR rows per block) against one
 exchange + all-reduce + launch per block; the default is
-min(8, slab rows // R).  The block engine is pluggable (`block=`) so the CPU
+min(4, slab rows // R) (the 2-4 sweeps per launch of the north star;
+tools/slab_projection.py measures a rank's block on one GPU).  The block engine is pluggable (`block=`) so the CPU
 tests drive the same host logic with an oracle engine on CPU tensors; the
 default engine is the CUDA one and there is no CPU fallback in the product.
 """
@@ -98,10 +99,10 @@ def _cuda_block(cfg: SolverConfig, tau: float, edge_preserving: bool):
 
 def default_sweeps_per_exchange(min_rows: int, halo: int, world: int, max_iters: int) -> int:
     """k of the temporal blocking: one block for a single rank; else at most
-    8 sweeps and never deeper than a neighbour's slab (k*R <= its rows)."""
+    4 sweeps and never deeper than a neighbour's slab (k*R <= its rows)."""
     if world == 1:
         return max(1, max_iters)
-    return max(1, min(8, min_rows // halo, max_iters))
+    return max(1, min(4, min_rows // halo, max_iters))
 
 
 class SlabSolver:

@@ -92,8 +92,8 @@ def test_slab_bounds_cover_the_image():
     assert halo_rows(25) == 12 and halo_rows(49) == 24 and halo_rows(1) == 1
     with pytest.raises(ValueError):
         slab_bounds(10, 2, 2)
-    # C4 at G = 8 (270 rows, R = 12): 8 sweeps per exchange; C5 (540, 24): 8
-    assert default_sweeps_per_exchange(270, 12, 8, 500) == 8
+    # C4 at G = 8 (270 rows, R = 12): 4 sweeps per exchange; C5 (540, 24): 4
+    assert default_sweeps_per_exchange(270, 12, 8, 500) == 4
     assert default_sweeps_per_exchange(30, 12, 8, 500) == 2
     assert default_sweeps_per_exchange(540, 24, 8, 3) == 3
     assert default_sweeps_per_exchange(10, 3, 1, 200) == 200
