@@ -217,6 +217,18 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
                               int32_t* failed_host, void* workspace, size_t workspace_bytes,
                               void* stream);
 
+/* pdz_fixed_point_solve without the host synchronisation: queues the solve
+ * on `stream` and, behind it, copies its outcome into the caller's DEVICE
+ * buffer `state` of pdz_solve_state_bytes(params) bytes: double
+ * norms[max_iters][P], then int32 iterations[P], converged[P], failed[P],
+ * abort[1] (1: a persistent-kernel dependency wait timed out).  The caller
+ * queues more work (clamp, result copy) and reads `state` once; dehaze()
+ * does.  Returns after queueing. */
+size_t pdz_solve_state_bytes(const pdz_solve_params* params);
+int32_t pdz_fixed_point_solve_async(const pdz_solve_params* params, const float* phi,
+                                    const float* lambda_map, float* u_out, void* state,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* Asynchronous fixed-iteration variant for benchmarking: exactly
  * params->max_iters sweeps (rel_tol ignored) captured in a CUDA graph,
  * norms left on the device in the workspace.  Returns immediately. */

@@ -89,6 +89,8 @@ _SIGNATURES = {
     "pdz_gaussian_f64": (_i32, [_pp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_step_workspace_bytes": (_sz, [_pp]),
     "pdz_fixed_point_step": (_i32, [_pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "pdz_solve_state_bytes": (_sz, [_pp]),
+    "pdz_fixed_point_solve_async": (_i32, [_pp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_fixed_point_sweeps_from": (
         _i32, [_pp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_fixed_point_step_rows": (_i32, [_pp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp,

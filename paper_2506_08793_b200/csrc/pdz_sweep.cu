@@ -1162,6 +1162,50 @@ int32_t pdz_fixed_point_solve(const pdz_solve_params* params, const float* phi,
   return PDZ_OK;
 }
 
+size_t pdz_solve_state_bytes(const pdz_solve_params* params) {
+  if (params == nullptr || params->planes < 1 || params->max_iters < 1) return 0;
+  return size_t(params->max_iters) * params->planes * sizeof(double) +
+         (3 * size_t(params->planes) + 1) * sizeof(int32_t);
+}
+
+__global__ void abort_flag_kernel(const int32_t* flags, int32_t* out) { out[0] = flags[1]; }
+
+int32_t pdz_fixed_point_solve_async(const pdz_solve_params* params, const float* phi,
+                                    const float* lambda_map, float* u_out, void* state,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  Plan pl;
+  int32_t rc = solve_plan(params, phi, lambda_map, &pl);
+  if (rc != PDZ_OK) return rc;
+  PDZ_REQUIRE(phi && lambda_map && u_out && state, "NULL array argument");
+  SolveLayout L = carve_solve(params, pl, workspace, workspace_bytes);
+  if (workspace == nullptr || L.bytes > workspace_bytes) {
+    set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
+    return PDZ_EWORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  // no host polling: the tiled fallback queues every chunk (stopped planes
+  // are skipped by the sweeps); the persistent kernel stops by itself
+  rc = queue_solve(params, pl, L, phi, lambda_map, u_out, s, false);
+  if (rc != PDZ_OK) return rc;
+  const size_t P = params->planes;
+  char* st = static_cast<char*>(state);
+  const size_t nb = size_t(params->max_iters) * P * sizeof(double);
+  int32_t* ints = reinterpret_cast<int32_t*>(st + nb);
+  PDZ_CUDA(cudaMemcpyAsync(st, L.st.norms, nb, cudaMemcpyDeviceToDevice, s), "state norms");
+  PDZ_CUDA(cudaMemcpyAsync(ints, L.st.iters, P * 4, cudaMemcpyDeviceToDevice, s), "state iters");
+  PDZ_CUDA(cudaMemcpyAsync(ints + P, L.st.converged, P * 4, cudaMemcpyDeviceToDevice, s),
+           "state converged");
+  PDZ_CUDA(cudaMemcpyAsync(ints + 2 * P, L.st.failed, P * 4, cudaMemcpyDeviceToDevice, s),
+           "state failed");
+  if (pl.stream) {
+    abort_flag_kernel<<<1, 1, 0, s>>>(L.sy.flags, ints + 3 * P);
+    PDZ_CHECK_LAUNCH("abort flag");
+  } else {
+    PDZ_CUDA(cudaMemsetAsync(ints + 3 * P, 0, 4, s), "abort flag");
+  }
+  return PDZ_OK;
+}
+
 int32_t pdz_fixed_point_sweeps_async(const pdz_solve_params* params, const float* phi,
                                      const float* lambda_map, void* workspace,
                                      size_t workspace_bytes, void* stream) {

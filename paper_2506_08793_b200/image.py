@@ -8,6 +8,8 @@ between the two worlds; the compute itself is always the CUDA library.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 
 __all__ = ["validate_image", "validate_unit_image", "validate_field", "clamp01",
@@ -43,11 +45,17 @@ def validate_image(image):
     return arr
 
 
-def validate_unit_image(image):
+_stats_pinned = threading.local()
+
+
+def validate_unit_image(image, defer: bool = False):
     """validate_image followed by the [0, 1] range check (scattering.py:41-45).
     Returns (image, range_check): the finiteness error is raised here, the
     range error by range_check() so callers keep the reference's check order.
-    Device tensors need ONE host read for both (finite, min, max)."""
+    Device tensors need ONE host read for both (finite, min, max).  With
+    `defer` (device tensors) that read is queued asynchronously and BOTH
+    errors are raised by range_check(), in the same order: the caller keeps
+    queueing device work meanwhile instead of stalling the GPU on the read."""
     if not is_device_array(image):
         arr = validate_image(image)
 
@@ -63,15 +71,34 @@ def validate_unit_image(image):
     if shape[0] < 1 or shape[1] < 1:
         raise ValueError(f"image dimensions must be >= 1, got shape {shape}")
     lo, hi = torch.aminmax(image)
-    stats = torch.stack((torch.isfinite(image).all().to(torch.float64), lo.to(torch.float64),
-                         hi.to(torch.float64))).to("cpu").tolist()
-    if stats[0] != 1.0:
-        raise ValueError("image contains non-finite values")
+    stats_dev = torch.stack((torch.isfinite(image).all().to(torch.float64),
+                             lo.to(torch.float64), hi.to(torch.float64)))
+    if not defer:
+        stats = stats_dev.to("cpu").tolist()
+        if stats[0] != 1.0:
+            raise ValueError("image contains non-finite values")
 
-    def check():
+        def check():
+            if stats[1] < 0.0 or stats[2] > 1.0:
+                raise ValueError("image values must lie in [0, 1]")
+        return image, check
+    # one pinned 3-double slot per thread, read behind an event
+    buf = getattr(_stats_pinned, "buf", None)
+    if buf is None:
+        buf = _stats_pinned.buf = torch.empty(3, dtype=torch.float64, pin_memory=True)
+        _stats_pinned.event = torch.cuda.Event()
+    buf.copy_(stats_dev, non_blocking=True)
+    ev = _stats_pinned.event
+    ev.record()
+
+    def deferred_check():
+        ev.synchronize()
+        stats = buf.tolist()
+        if stats[0] != 1.0:
+            raise ValueError("image contains non-finite values")
         if stats[1] < 0.0 or stats[2] > 1.0:
             raise ValueError("image values must lie in [0, 1]")
-    return image, check
+    return image, deferred_check
 
 
 def validate_field(field):

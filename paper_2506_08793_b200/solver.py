@@ -23,6 +23,8 @@ from __future__ import annotations
 import csv
 import logging
 
+import threading
+
 import numpy as np
 
 from . import _native as nat
@@ -268,54 +270,81 @@ def solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=
                   tau=None, warn=True):
     """fixed_point_solve for every plane at once.  Returns (u [P][H][W] float32
     device tensor, [SolverTrace] * P)."""
+    u, finish = queue_solve_problem(problem, cfg, edge_preserving=edge_preserving, tau=tau,
+                                    warn=warn)
+    return u, finish()
+
+
+_solve_pinned = threading.local()
+
+
+def queue_solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_preserving=True,
+                        tau=None, warn=True):
+    """Queue the solve of every plane (pdz_fixed_point_solve_async) and the
+    copy of its outcome (norms, iterations, flags, tau bounds) to pinned host
+    memory.  Returns (u, finish): u is the device result, valid for work
+    queued after this call on the current stream; finish() waits for the
+    outcome only, raises the reference's errors and warning (solver.py:335-350)
+    and returns the [SolverTrace] * P."""
     import torch
 
     step = cfg.tau if tau is None else float(tau)
+    P = problem.planes
     bounds = problem.bounds if problem.bounds is not None else _tau_bounds(problem, cfg,
                                                                           cfg.epsilon)
-    host_bounds = [None]
-
-    def check_bounds():  # solver.py:335-339; device bounds are read after the solve
-        if host_bounds[0] is None:
-            hb = bounds.to("cpu").numpy() if hasattr(bounds, "is_cuda") else np.asarray(bounds)
-            host_bounds[0] = hb
-            if warn:
-                for b in hb:
-                    if step > b:
-                        logger.warning(
-                            "relaxation step %.3g exceeds the stability bound %.3g at the "
-                            "initial iterate; convergence is not guaranteed", step, b)
-        return host_bounds[0]
-
-    if not hasattr(bounds, "is_cuda"):
-        check_bounds()
-    P = problem.planes
     prm = _params(problem.height, problem.width, P, problem.channels, cfg,
                   edge_preserving=edge_preserving, tau=step)
     lib = nat.lib()
     ws = nat.workspace(lib.pdz_solve_workspace_bytes(prm), "solve")
+    nbytes = int(lib.pdz_solve_state_bytes(prm))
+    state = nat.workspace(nbytes, "solve-state")
     u = torch.empty_like(problem.phi)
-    norms = np.zeros((cfg.max_iters, P), dtype=np.float64)
-    iters = np.zeros(P, dtype=np.int32)
-    conv = np.zeros(P, dtype=np.int32)
-    failed = np.zeros(P, dtype=np.int32)
-    rc = lib.pdz_fixed_point_solve(prm, nat.ptr(problem.phi), nat.ptr(problem.lam), nat.ptr(u),
-                                   norms.ctypes.data, iters.ctypes.data, conv.ctypes.data,
-                                   failed.ctypes.data, nat.ptr(ws), ws.numel(),
-                                   nat.stream_ptr())
-    bounds = check_bounds()
-    if rc == nat.PDZ_ENONFINITE:
-        first = int(np.flatnonzero(failed)[0])
-        raise FloatingPointError(
-            f"solver produced non-finite values at iteration {int(failed[first])}")
-    nat.check(rc)
-    traces = []
-    for p in range(P):
-        n = int(iters[p])
-        traces.append(SolverTrace(residual_norms=[float(v) for v in norms[:n, p]],
-                                  iterations_run=n, converged=bool(conv[p]), tau_used=step,
-                                  tau_bound=float(bounds[p])))
-    return u, traces
+    nat.check(lib.pdz_fixed_point_solve_async(prm, nat.ptr(problem.phi), nat.ptr(problem.lam),
+                                              nat.ptr(u), nat.ptr(state), nat.ptr(ws),
+                                              ws.numel(), nat.stream_ptr()))
+    # one pinned landing buffer per thread: the outcome, then the bounds
+    nb_host = nbytes + 8 * P
+    buf = getattr(_solve_pinned, "buf", None)
+    if buf is None or buf.numel() < nb_host:
+        buf = _solve_pinned.buf = torch.empty(max(nb_host, 4096), dtype=torch.uint8,
+                                              pin_memory=True)
+        _solve_pinned.event = torch.cuda.Event()
+    buf[:nbytes].copy_(state[:nbytes], non_blocking=True)
+    dev_bounds = hasattr(bounds, "is_cuda")
+    if dev_bounds:
+        buf[nbytes:nb_host].copy_(bounds.contiguous().view(torch.uint8), non_blocking=True)
+    ev = _solve_pinned.event
+    ev.record()
+
+    def finish():
+        ev.synchronize()
+        raw = buf[:nb_host].numpy()
+        norms = raw[:8 * cfg.max_iters * P].view(np.float64).reshape(cfg.max_iters, P)
+        ints = raw[8 * cfg.max_iters * P:nbytes].view(np.int32)
+        iters, conv, failed, abort = ints[:P], ints[P:2 * P], ints[2 * P:3 * P], ints[3 * P]
+        hb = (raw[nbytes:nb_host].view(np.float64).copy() if dev_bounds
+              else np.asarray(bounds, dtype=np.float64))
+        if warn:  # solver.py:335-339
+            for b in hb:
+                if step > b:
+                    logger.warning(
+                        "relaxation step %.3g exceeds the stability bound %.3g at the "
+                        "initial iterate; convergence is not guaranteed", step, b)
+        if abort:
+            raise RuntimeError("persistent sweep aborted: a CTA dependency wait timed out")
+        bad = np.flatnonzero(failed)
+        if bad.size:
+            raise FloatingPointError(
+                f"solver produced non-finite values at iteration {int(failed[bad[0]])}")
+        traces = []
+        for p in range(P):
+            n = int(iters[p])
+            traces.append(SolverTrace(residual_norms=[float(v) for v in norms[:n, p]],
+                                      iterations_run=n, converged=bool(conv[p]), tau_used=step,
+                                      tau_bound=float(hb[p])))
+        return traces
+
+    return u, finish
 
 
 def _lambda_mode(flags, cfg) -> int:
@@ -442,14 +471,22 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
     cfg = cfg or SolverConfig()
     flags = normalize_ablation(ablation)
     # torch inputs (pinned host or device) are moved first and validated on the
-    # GPU with one combined reduction (finite, min, max: one host read)
-    img, unit_check = validate_unit_image(to_device(image) if is_device_array(image) else image)
+    # GPU with one combined reduction (finite, min, max); its host read is
+    # deferred until the front end is queued, so the GPU never waits for the
+    # host in between (the errors are the same and come before any result)
+    dev_in = is_device_array(image)
+    img, unit_check = validate_unit_image(to_device(image) if dev_in else image, defer=dev_in)
     if workers < 1:
+        if dev_in:
+            unit_check()  # the finiteness error comes first, as in the reference
         raise ValueError("workers must be >= 1")
-    unit_check()
+    if not dev_in:
+        unit_check()
     img_dev, is_f64 = _image_dev(img)
     h, w, c = img_dev.shape
     t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
+    if dev_in:
+        unit_check()
     lib = nat.lib()
     if "no-pde" in flags:
         phi64 = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
@@ -467,10 +504,14 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
     # solve runs
     t_host, a_host = to_host_async(t_dev, image), to_host_async(a_dev, image)
     problem = DeviceProblem(phi, lam, h, w, c, c, bounds)
-    u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    # clamp + interleave and the result copy are queued behind the solve
+    # before the host reads the solve's outcome: the GPU never waits for it
+    u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
     nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1, nat.stream_ptr()))
-    return (to_host(out, image), DehazeResult(a_host(), t_host(), traces, flags))
+    out_host = to_host_async(out, image)
+    traces = finish()
+    return (out_host(), DehazeResult(a_host(), t_host(), traces, flags))
 
 
 def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):

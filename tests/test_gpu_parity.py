@@ -449,6 +449,20 @@ def test_device_tensor_path(pdz):
                           ablation=("no-multiscale", "no-guided"))
     assert o_t.is_cuda
     np.testing.assert_array_equal(o_t.cpu().numpy(), o_np)
+    # device and pinned-host tensors: the validation read is deferred behind
+    # the queued front end, with the reference's errors and their order
+    for bad, msg in ((np.nan, "non-finite"), (1.5, r"\[0, 1\]"), (-0.1, r"\[0, 1\]")):
+        x = img.copy()
+        x[3, 4, 0] = bad
+        for t in (torch.from_numpy(x).cuda(), torch.from_numpy(x).pin_memory()):
+            with pytest.raises(ValueError, match=msg):
+                pdz.dehaze(t, cfg, ablation=("no-multiscale", "no-guided"))
+    x = img.copy()
+    x[0, 0, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        pdz.dehaze(torch.from_numpy(x).cuda(), cfg, workers=0)
+    with pytest.raises(ValueError, match="workers"):
+        pdz.dehaze(torch.from_numpy(img).cuda(), cfg, workers=0)
 
 
 @pytest.mark.parametrize("shape,k,edge", [((400, 136), 19, True), ((333, 128), 13, True),
