@@ -57,7 +57,7 @@ namespace pdz {
 constexpr int kSTW = 64;                    // strip width (output columns)
 // Block geometry V (a template parameter of the kernel, picked per solve from
 // the partition, pdz_sweep.cu):
-//  V = 0: 19 compute warps x 6 output rows (114-row blocks; 4 rows / 76 for
+//  V = 0: 19 compute warps x 6 output rows (114-row blocks; 5 rows / 95 for
 //         R = 24, whose wider staging would not fit shared memory otherwise),
 //         20 warps x 96 registers (5 warps per SM sub-partition fill its
 //         16K-register file).  Best when a CTA's rows of a strip fit one block
@@ -67,7 +67,13 @@ constexpr int kSTW = 64;                    // strip width (output columns)
 //         (configs 3 and 4): fewer blocks per strip and more registers per
 //         thread for the vertical pass.
 __host__ __device__ constexpr int geo_scw(int V) { return V ? 15 : 19; }
-__host__ __device__ constexpr int geo_rpw(int R, int V) { return V ? 8 : (R <= 12 ? 6 : 4); }
+// R = 24: 5 rows per warp (95-row blocks, 215 KB of shared memory); 4 rows
+// (76-row blocks) cost 9 % more per sweep on config 5 (1.63x horizontal-pass
+// rows per output row instead of 1.51x, 1024 H items on 608 threads).
+#ifndef PDZ_RPW24
+#define PDZ_RPW24 5
+#endif
+__host__ __device__ constexpr int geo_rpw(int R, int V) { return V ? 8 : (R <= 12 ? 6 : PDZ_RPW24); }
 __host__ __device__ constexpr int geo_srb(int R, int V) { return geo_scw(V) * geo_rpw(R, V); }
 __host__ __device__ constexpr int geo_threads(int V) { return (geo_scw(V) + 1) * 32; }  // + service warp
 __host__ __device__ constexpr int geo_nreg(int V) { return V ? 128 : 96; }
@@ -931,6 +937,10 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
       constexpr int SL = Gm::RP <= 16 ? 16 : 32;  // pad-column slots per row
       static_assert(Gm::RP <= SL, "pad columns per row slot");
       const int k = tid % SL;
+      // every staged row is patched, so the second TMA box must have landed
+      // first (else it overwrites the reflected columns with the NaN pads)
+      mbar_wait(&bars[5 + ib], par);
+      got2 = true;
       if (k < Gm::RP && xr + k < Gm::PWD)
         for (int sr = tid / SL; sr < hn; sr += kComputeThreads / SL)
           in_cur[sr * Gm::PITCH + xr + k] = in_cur[sr * Gm::PITCH + xr - 1 - k];

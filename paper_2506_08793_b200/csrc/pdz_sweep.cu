@@ -773,6 +773,11 @@ __global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict
     const int y = int((i / wp) % hp) - pr, x = int(i % wp) - pc;
     if (y >= 0 && y < H && x >= 0 && x < W) {
       buf[i] = phi[(pl * H + y) * W + x];
+#ifdef PDZ_POISON_ALL
+      const float nan = __int_as_float(0x7fc00000);
+      if (buf1) buf1[i] = nan;
+      if (buf2) buf2[i] = nan;
+#endif
     } else {
       const float nan = __int_as_float(0x7fc00000);
       buf[i] = nan;

@@ -41,11 +41,15 @@ def peak():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=40)
+    ap.add_argument("--only", default="", help="comma-separated config numbers (1-5)")
     args = ap.parse_args()
     lib = nat.lib()
     flags = frozenset(("no-multiscale", "no-guided"))
     pk = peak()
-    for name, h, w, nimg, k, sigma, pr, full_iters in CONFIGS:
+    only = {int(x) for x in args.only.split(",") if x}
+    for ci, (name, h, w, nimg, k, sigma, pr, full_iters) in enumerate(CONFIGS, 1):
+        if only and ci not in only:
+            continue
         iters = min(args.iters, full_iters)
         cfg = pdz.SolverConfig(tau=TAU, sigma=sigma, kernel_size=k, patch_radius=pr,
                                max_iters=iters, rel_tol=1e-300)
