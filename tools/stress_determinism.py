@@ -16,6 +16,18 @@ CASES = [((600, 3000), 13), ((600, 3840), 25), ((300, 7680), 49), ((400, 136), 1
          ((333, 128), 13), ((1024, 1024), 19), ((96, 128), 13), ((5, 3), 49)]
 
 
+def _dz(res):
+    out, info = res
+    return (np.asarray(out).tobytes() + np.asarray(info.airlight).tobytes()
+            + np.asarray(info.transmission).tobytes()
+            + b"".join(np.asarray(t.residual_norms).tobytes() for t in info.traces))
+
+
+def _dzb(res):
+    out, infos = res
+    return np.asarray(out).tobytes() + b"".join(_dz((np.empty(0), i)) for i in infos)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=30)
@@ -29,6 +41,20 @@ def main():
         cfg = pdz.SolverConfig(tau=TAU, kernel_size=k, sigma=k / 6.0, max_iters=args.iters,
                                rel_tol=1e-300)
         probs.append((f"{h}x{w} K={k}", ch, t, cfg))
+    from paper_2506_08793_b200.synthetic import make_hazy_scene
+    abl = ("no-multiscale", "no-guided")
+    extra = []  # (name, callable returning bytes to compare)
+    for h, w in [(256, 320), (200, 300)]:
+        img = make_hazy_scene(h, w, 3, 1).hazy.astype(np.float64)
+        cfg = pdz.SolverConfig(tau=TAU, kernel_size=19, sigma=3.0, max_iters=10, rel_tol=1e-300)
+        extra.append((f"dehaze {h}x{w}", lambda img=img, cfg=cfg: _dz(pdz.dehaze(img, cfg, abl))))
+    img = make_hazy_scene(160, 200, 3, 2).hazy.astype(np.float64)
+    cfg_stop = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=80, rel_tol=5e-3)
+    extra.append(("dehaze stop-rule 160x200",
+                  lambda: _dz(pdz.dehaze(img, cfg_stop, ("no-multiscale", "no-guided")))))
+    batch = [make_hazy_scene(120, 200, 3, 10 + i).hazy.astype(np.float64) for i in range(4)]
+    cfg_b = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=8, rel_tol=1e-300)
+    extra.append(("dehaze_batch 4x120x200", lambda: _dzb(pdz.dehaze_batch(batch, cfg_b, abl))))
     first = {}
     bad = 0
     for rep in range(args.reps):
@@ -46,7 +72,19 @@ def main():
                 d = np.max(np.abs(np.frombuffer(key[0]) - np.frombuffer(first[name][0])))
                 print(f"rep {rep} {name}: differs from the first solve (max {d:.3e})", flush=True)
                 bad += 1
-    print(f"stress: {args.reps} reps x {len(probs)} problems, {bad} bad", flush=True)
+        for name, fn in extra:
+            try:
+                key = fn()
+            except Exception as e:  # noqa: BLE001
+                print(f"rep {rep} {name}: {type(e).__name__}: {e}", flush=True)
+                bad += 1
+                continue
+            if name not in first:
+                first[name] = key
+            elif key != first[name]:
+                print(f"rep {rep} {name}: differs from the first run", flush=True)
+                bad += 1
+    print(f"stress: {args.reps} reps x {len(probs) + len(extra)} problems, {bad} bad", flush=True)
     return 1 if bad else 0
 
 
