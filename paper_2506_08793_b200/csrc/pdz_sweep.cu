@@ -762,48 +762,79 @@ __global__ void sync_init_kernel(Sync sy, int G) {
 // readers reflect image borders themselves, so the pads of every iterate
 // buffer are poisoned with NaN: a read of a pad as data would surface as a
 // non-finite result instead of a silent error.
+// One CTA per padded row (grid-stride over the P * (H + 2 pr) rows), float4
+// columns when every row and the pad width are 16-byte multiples (vec): the
+// index arithmetic is per row, not per element (per-element 64-bit divides
+// made these copies run at ~1.3 TB/s).
 __global__ void pad_init_kernel(const float* __restrict__ phi, float* __restrict__ buf,
                                 float* __restrict__ buf1, float* __restrict__ buf2, int H, int W,
-                                int P, int pr, int pc) {
+                                int P, int pr, int pc, int vec) {
   const int wp = W + 2 * pc, hp = H + 2 * pr;
-  const int64_t n = int64_t(P) * hp * wp;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t pl = i / (int64_t(hp) * wp);
-    const int y = int((i / wp) % hp) - pr, x = int(i % wp) - pc;
-    if (y >= 0 && y < H && x >= 0 && x < W) {
-      buf[i] = phi[(pl * H + y) * W + x];
+  const float nan = __int_as_float(0x7fc00000);
 #ifdef PDZ_POISON_ALL
-      const float nan = __int_as_float(0x7fc00000);
-      if (buf1) buf1[i] = nan;
-      if (buf2) buf2[i] = nan;
+  constexpr bool kPoisonAll = true;
+#else
+  constexpr bool kPoisonAll = false;
 #endif
+  const int64_t rows = int64_t(P) * hp;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t pl = r / hp;
+    const int y = int(r - pl * hp) - pr;
+    const bool in_row = y >= 0 && y < H;
+    const float* src = phi + (pl * H + (in_row ? y : 0)) * W;
+    float* d0 = buf + r * wp;
+    float* d1 = buf1 ? buf1 + r * wp : nullptr;
+    float* d2 = buf2 ? buf2 + r * wp : nullptr;
+    if (vec) {
+      const float4 nan4 = make_float4(nan, nan, nan, nan);
+      for (int c = threadIdx.x; c < wp / 4; c += blockDim.x) {
+        const int x = 4 * c - pc;
+        const bool in = in_row && x >= 0 && x < W;
+        reinterpret_cast<float4*>(d0)[c] = in ? *reinterpret_cast<const float4*>(src + x) : nan4;
+        if (!in || kPoisonAll) {
+          if (d1) reinterpret_cast<float4*>(d1)[c] = nan4;
+          if (d2) reinterpret_cast<float4*>(d2)[c] = nan4;
+        }
+      }
     } else {
-      const float nan = __int_as_float(0x7fc00000);
-      buf[i] = nan;
-      if (buf1) buf1[i] = nan;
-      if (buf2) buf2[i] = nan;
+      for (int c = threadIdx.x; c < wp; c += blockDim.x) {
+        const int x = c - pc;
+        const bool in = in_row && x >= 0 && x < W;
+        d0[c] = in ? src[x] : nan;
+        if (!in || kPoisonAll) {
+          if (d1) d1[c] = nan;
+          if (d2) d2[c] = nan;
+        }
+      }
     }
   }
 }
 
-// Dense final iterate: plane p from buf[iters[p] & 1] (the last iteration whose
-// norm was recorded; solver.py:359), interior of the padded layout.
+// Dense final iterate: plane p from buf[iters[p] % nbuf] (the last iteration
+// whose norm was recorded; solver.py:359), interior of the padded layout.  One
+// CTA per output row, float4 columns when aligned (vec).
 __global__ void extract_kernel(const float* __restrict__ buf0, const float* __restrict__ buf1,
                                const float* __restrict__ buf2, int nbuf,
                                const int32_t* __restrict__ iters, float* __restrict__ out, int H,
-                               int W, int P, int pr, int pc) {
+                               int W, int P, int pr, int pc, int vec) {
   const int wp = W + 2 * pc, hp = H + 2 * pr;
-  const int64_t n = int64_t(P) * H * W;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t pl = i / (int64_t(H) * W);
-    const int y = int((i / W) % H), x = int(i % W);
+  const int64_t rows = int64_t(P) * H;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t pl = r / H;
+    const int y = int(r - pl * H);
     const int k = iters[pl] % nbuf;
-    const float* src = k == 0 ? buf0 : (k == 1 ? buf1 : buf2);
-    out[i] = src[(pl * hp + y + pr) * wp + x + pc];
+    const float* src = (k == 0 ? buf0 : (k == 1 ? buf1 : buf2)) + (pl * hp + y + pr) * wp + pc;
+    float* dst = out + r * W;
+    if (vec) {
+      for (int c = threadIdx.x; c < W / 4; c += blockDim.x)
+        reinterpret_cast<float4*>(dst)[c] = reinterpret_cast<const float4*>(src)[c];
+    } else {
+      for (int c = threadIdx.x; c < W; c += blockDim.x) dst[c] = src[c];
+    }
   }
 }
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct SolveLayout {
   float* buf0;  // iterate buffers: tiled ping-pong / persistent triple (padded)
@@ -917,11 +948,13 @@ static void time_mark(int which, cudaStream_t s) {
 
 static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
                              float* out, cudaStream_t s) {
-  const int64_t n = int64_t(p->planes) * p->height * p->width;
-  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  const int64_t rows = int64_t(p->planes) * p->height;
+  const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms()) * 16));
+  const int vec = p->width % 4 == 0 && pl.pad_c % 4 == 0 && aligned16(out) &&
+                  aligned16(L.buf0) && aligned16(L.buf1) && (!L.buf2 || aligned16(L.buf2));
   extract_kernel<<<blocks, 256, 0, s>>>(L.buf0, L.buf1, L.buf2, pl.stream ? kNBuf : 2,
                                         L.st.iters, out, p->height, p->width,
-                                        p->planes, pl.pad_r, pl.pad_c);
+                                        p->planes, pl.pad_r, pl.pad_c, vec);
   PDZ_CHECK_LAUNCH("extract");
   return PDZ_OK;
 }
@@ -941,10 +974,13 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   la.tile.cnt_hi = la.stream.cnt_hi = cnt_hi;
   if (u_init == nullptr) u_init = phi;
   {
-    const int64_t n = int64_t(p->planes) * (p->height + 2 * pl.pad_r) * (p->width + 2 * pl.pad_c);
-    const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    const int64_t rows = int64_t(p->planes) * (p->height + 2 * pl.pad_r);
+    const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms()) * 16));
+    const int vec = p->width % 4 == 0 && pl.pad_c % 4 == 0 && aligned16(u_init) &&
+                    aligned16(L.buf0) && aligned16(L.buf1) && (!L.buf2 || aligned16(L.buf2));
     pad_init_kernel<<<blocks, 256, 0, s>>>(u_init, L.buf0, pl.stream ? L.buf1 : nullptr, L.buf2,
-                                           p->height, p->width, p->planes, pl.pad_r, pl.pad_c);
+                                           p->height, p->width, p->planes, pl.pad_r, pl.pad_c,
+                                           vec);
     PDZ_CHECK_LAUNCH("u0 = Phi");
   }
   init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
