@@ -55,6 +55,12 @@ def main():
     batch = [make_hazy_scene(120, 200, 3, 10 + i).hazy.astype(np.float64) for i in range(4)]
     cfg_b = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=8, rel_tol=1e-300)
     extra.append(("dehaze_batch 4x120x200", lambda: _dzb(pdz.dehaze_batch(batch, cfg_b, abl))))
+    # planes of a batch that stop at different iterations (frozen planes are
+    # skipped by CTA ranges that cross image boundaries)
+    batch_s = [make_hazy_scene(100, 200, 3, 20 + i).hazy.astype(np.float64) for i in range(6)]
+    cfg_bs = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=120, rel_tol=2e-3)
+    extra.append(("dehaze_batch stop-rule 6x100x200",
+                  lambda: _dzb(pdz.dehaze_batch(batch_s, cfg_bs, abl))))
     first = {}
     bad = 0
     for rep in range(args.reps):
