@@ -3,6 +3,7 @@
 // (:266-277).  These are probes / one-off diagnostics, not the sweep: they
 // are templated on the scalar type so the numpy-facing API can evaluate them
 // in float64 exactly like the reference.
+#include <type_traits>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -158,6 +159,77 @@ __global__ void tau_scan_kernel(const TU* __restrict__ u, const TL* __restrict__
   }
 }
 
+// Interleaved (H, W, C) field, C <= 4: one pass over the pixels with every
+// channel handled by the same thread (the per-plane scan read the whole
+// interleaved array once per channel).  The same per-face arithmetic as
+// tau_scan_kernel; min / max reductions are order-independent, so the bounds
+// are bitwise those of the per-plane scan.
+template <typename TL>
+__global__ void tau_scan_hwc_kernel(const double* __restrict__ u, const TL* __restrict__ lam,
+                                    int H, int W, int C, unsigned long long* smin,
+                                    unsigned long long* lmax) {
+  double best[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+  double lbest = -INFINITY;
+  const size_t n = size_t(H) * W;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int y = int(i / W), x = int(i - size_t(y) * W);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= C) break;
+      auto at = [&](size_t j) -> double { return u[j * C + c]; };
+      auto cy = [&](int xx) -> double {
+        const size_t j = size_t(y) * W + xx;
+        if (y == 0) return at(j + W) - at(j);
+        if (y == H - 1) return at(j) - at(j - W);
+        return (at(j + W) - at(j - W)) / 2.0;
+      };
+      auto cx = [&](int yy) -> double {
+        const size_t j = size_t(yy) * W + x;
+        if (x == 0) return at(j + 1) - at(j);
+        if (x == W - 1) return at(j) - at(j - 1);
+        return (at(j + 1) - at(j - 1)) / 2.0;
+      };
+      const double cv = at(i);
+      if (x < W - 1) {
+        const double jump = at(i + 1) - cv;
+        const double along = 0.5 * (cy(x + 1) + cy(x));
+        best[c] = fmin(best[c], jump * jump + along * along);
+      }
+      if (y < H - 1) {
+        const double jump = at(i + W) - cv;
+        const double along = 0.5 * (cx(y + 1) + cx(y));
+        best[c] = fmin(best[c], jump * jump + along * along);
+      }
+    }
+    lbest = fmax(lbest, double(lam[i]));
+  }
+  __shared__ double sb[4][32];
+  __shared__ double sl[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    for (int o = 16; o > 0; o >>= 1) best[c] = fmin(best[c], __shfl_xor_sync(0xffffffffu, best[c], o));
+  for (int o = 16; o > 0; o >>= 1) lbest = fmax(lbest, __shfl_xor_sync(0xffffffffu, lbest, o));
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sb[c][warp] = best[c];
+    sl[warp] = lbest;
+  }
+  __syncthreads();
+  if (threadIdx.x < C) {
+    const int c = threadIdx.x;
+    double b = sb[c][0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) b = fmin(b, sb[c][w]);
+    atomic_min_u64(&smin[c], static_cast<unsigned long long>(__double_as_longlong(b)));
+  }
+  if (threadIdx.x == 0) {
+    double l = sl[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) l = fmax(l, sl[w]);
+    atomicMax(&lmax[0], static_cast<unsigned long long>(f64_order_key(l)));
+  }
+}
+
 __global__ void tau_final_kernel(const unsigned long long* smin, const unsigned long long* lmax,
                                  int P, int C, double eps, double* bound) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,8 +314,17 @@ static int32_t run_tau(const pdz_solve_params* prm, const TU* u, const TL* lam, 
   const size_t n = size_t(prm->height) * prm->width;
   const int bx = int(std::min<size_t>((n + 255) / 256, size_t(4 * num_sms())));
   const size_t us = interleaved ? size_t(P) : 1, ps = interleaved ? 1 : n;
-  tau_scan_kernel<TU, TL><<<dim3(bx, P), 256, 0, s>>>(u, lam, prm->height, prm->width,
-                                                      prm->channels, us, ps, smin, lmax);
+  if constexpr (std::is_same<TU, double>::value) {
+    if (interleaved && P == prm->channels && P <= 4) {
+      tau_scan_hwc_kernel<TL><<<bx, 256, 0, s>>>(u, lam, prm->height, prm->width, P, smin, lmax);
+    } else {
+      tau_scan_kernel<TU, TL><<<dim3(bx, P), 256, 0, s>>>(u, lam, prm->height, prm->width,
+                                                          prm->channels, us, ps, smin, lmax);
+    }
+  } else {
+    tau_scan_kernel<TU, TL><<<dim3(bx, P), 256, 0, s>>>(u, lam, prm->height, prm->width,
+                                                        prm->channels, us, ps, smin, lmax);
+  }
   tau_final_kernel<<<(P + 255) / 256, 256, 0, s>>>(smin, lmax, P, prm->channels,
                                                    prm->epsilon, bound);
   PDZ_CHECK_LAUNCH("tau bound");
