@@ -262,6 +262,17 @@ int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);
  * H >= 2R, W >= 2 ceil4(R), a compiled radius, every CTA co-resident),
  * 1 = tiled fallback, -1 = invalid params. */
 int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params);
+/* The launch plan `params` gets (host call, no device work), for tests and
+ * benchmarks: info_host[0..n) <- {kind (2 persistent / 1 tiled), CTAs (G,
+ * or tiles for the tiled kernel), CTAs per strip (kps; 0 = even split of
+ * strip-rows, ranges may span strips and images), border bonus, block
+ * geometry V, radius R, partial slots per plane, strips per image, output
+ * rows per block, threads per CTA, stop rule armed}. */
+#define PDZ_PLAN_INFO_LEN 11
+int32_t pdz_solve_plan_info(const pdz_solve_params* params, int32_t* info_host, int32_t n);
+/* Name of the sweep kernel template `params` launches (e.g.
+ * "pdz::stream_kernel<9, 0, 1, 1>"), NUL-terminated into buf_host[n]. */
+int32_t pdz_solve_kernel_name(const pdz_solve_params* params, char* buf_host, int32_t n);
 /* Device pointer to the plane-p final iterate (dense [H][W]) inside a solve
  * workspace after pdz_fixed_point_sweeps_async (`iterations` is ignored: the
  * solve already copied every plane's final iterate into the dense area). */

@@ -34,6 +34,7 @@ reference so that results are bitwise identical:
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -64,6 +65,9 @@ __all__ = [
     "guided_smooth",
     "luminance_refine",
     "run_pipeline",
+    "native_lib",
+    "solve_planes_native",
+    "relaxed_solve_native",
 ]
 
 # tests/conftest.py:12 of the reference -- the step every parity run pins.
@@ -441,9 +445,11 @@ def luminance_refine(img, t_raw, radius=30, reg=1e-3):
 # Whole pipeline  (solver.py:375-436)
 # --------------------------------------------------------------------------
 
-def run_pipeline(image, settings, ablation=(), separable=False, channel_workers=1):
+def run_pipeline(image, settings, ablation=(), separable=False, channel_workers=1,
+                 native=False):
     """Front end -> per-channel relaxed solve -> clamp.  Returns
-    (restored, airlight, transmission, traces)."""
+    (restored, airlight, transmission, traces).  native=True runs the solve
+    loop in the C restatement (relaxed_solve_native)."""
     flags = frozenset((ablation,) if isinstance(ablation, str) else ablation)
     img = np.asarray(image, dtype=np.float64)
     channels = img.shape[2]
@@ -470,6 +476,9 @@ def run_pipeline(image, settings, ablation=(), separable=False, channel_workers=
     edge = "no-edge" not in flags
 
     def one(c):
+        if native:
+            return relaxed_solve_native(img[:, :, c], t, float(airlight[c]), settings, lam,
+                                        edge)
         return relaxed_solve(img[:, :, c], t, float(airlight[c]), settings, lam, edge,
                              None, separable)
 
@@ -481,3 +490,85 @@ def run_pipeline(image, settings, ablation=(), separable=False, channel_workers=
         solved = [one(c) for c in range(channels)]
     out = np.clip(np.stack([u for u, _ in solved], axis=2), 0.0, 1.0)
     return out, airlight, t, [tr for _, tr in solved]
+
+
+# --------------------------------------------------------------------------
+# C restatement of the solve loop (oracle/pdz_oracle_solve.c)
+# --------------------------------------------------------------------------
+
+_NATIVE = None
+NATIVE_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build",
+                          "liboracle_solve.so")
+
+
+def native_lib():
+    """ctypes handle of oracle/_build/liboracle_solve.so (built by
+    __graft_entry__.build(); test infrastructure like the rest of oracle/)."""
+    global _NATIVE
+    if _NATIVE is None:
+        import ctypes
+
+        lib = ctypes.CDLL(NATIVE_LIB)
+        d, i = ctypes.c_double, ctypes.c_int
+        vp = ctypes.c_void_p
+        lib.oracle_relaxed_solve.argtypes = [vp, vp, i, i, i, i, i, d, d, d, i, i, d, vp, vp, vp,
+                                             vp, i]
+        lib.oracle_relaxed_solve.restype = i
+        lib.oracle_max_threads.restype = i
+        _NATIVE = lib
+    return _NATIVE
+
+
+def solve_planes_native(src, lam, settings, edge_preserving=True, tau=None, max_iters=None,
+                        rel_tol=None, threads=None):
+    """Relaxed solve of P planes from u0 = src (solver.py:324-359) in C.
+    src: (P, H, W) float64; lam: (H, W) shared by every plane or (P / k, H, W)
+    with k planes per map.  Returns (u (P, H, W), norms (iters, P) list per
+    plane, iterations_run [P], converged [P])."""
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    if src.ndim == 2:
+        src = src[None]
+    P, H, W = src.shape
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    if lam.ndim == 2:
+        lam = lam[None]
+    lam_div = P // lam.shape[0]
+    iters_max = settings.max_iters if max_iters is None else int(max_iters)
+    tol = settings.rel_tol if rel_tol is None else float(rel_tol)
+    step = settings.tau if tau is None else float(tau)
+    lib = native_lib()
+    u = np.empty_like(src)
+    norms = np.zeros((iters_max, P), dtype=np.float64)
+    iters = np.zeros(P, dtype=np.int32)
+    conv = np.zeros(P, dtype=np.int32)
+    nt = lib.oracle_max_threads() if threads is None else int(threads)
+    rc = lib.oracle_relaxed_solve(src.ctypes.data, lam.ctypes.data, P, lam_div, H, W,
+                                  settings.kernel_size, settings.sigma, settings.epsilon, step,
+                                  1 if edge_preserving else 0, iters_max, tol, u.ctypes.data,
+                                  norms.ctypes.data, iters.ctypes.data, conv.ctypes.data, nt)
+    if rc < 0:
+        raise ValueError("invalid solve arguments")
+    if rc > 0:
+        raise FloatingPointError(f"solver produced non-finite values at iteration {rc}")
+    return u, [norms[:iters[p], p].tolist() for p in range(P)], iters.tolist(), \
+        [bool(c) for c in conv]
+
+
+def relaxed_solve_native(channel, t, a_c, settings, lambda_map=None, edge_preserving=True,
+                         tau=None, threads=None):
+    """relaxed_solve with the sweep loop in C (same inputs, same OracleTrace)."""
+    chan = np.asarray(channel, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)
+    src = (chan - a_c * (1.0 - t)) / np.maximum(t, settings.t_floor)
+    if lambda_map is None:
+        lam = haze_weight(t, settings.lambda0, settings.beta, settings.lambda_monotonicity)
+    else:
+        lam = np.asarray(lambda_map, dtype=np.float64)
+    step = settings.tau if tau is None else float(tau)
+    trace = OracleTrace(step, stability_bound(src, lam, settings.epsilon))
+    u, norms, iters, conv = solve_planes_native(src, lam, settings, edge_preserving, step,
+                                                threads=threads)
+    trace.residual_norms = norms[0]
+    trace.iterations_run = iters[0]
+    trace.converged = conv[0]
+    return u[0], trace

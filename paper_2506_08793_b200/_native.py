@@ -104,6 +104,8 @@ _SIGNATURES = {
     "pdz_last_sweep_kernel_ms": (ctypes.c_float, []),
     "pdz_solve_kernel_launches": (_i64, [_pp]),
     "pdz_sweep_kernel_kind": (_i32, [_pp]),
+    "pdz_solve_plan_info": (_i32, [_pp, _vp, _i32]),
+    "pdz_solve_kernel_name": (_i32, [_pp, ctypes.c_char_p, _i32]),
     "pdz_clamp_interleave": (_i32, [_vp, _i32, _i32, _i32, _vp, _i32, _vp]),
     "pdz_quantize_u8": (_i32, [_vp, ctypes.c_int64, _vp, _vp, _vp]),
     "pdz_synthesize_haze": (_i32, [_vp, _vp, _vp, ctypes.c_int64, _i32, _vp, _vp]),
@@ -152,6 +154,24 @@ def check(rc: int) -> None:
     if rc in (PDZ_EINVAL, PDZ_EWORKSPACE):
         raise ValueError(msg)
     raise RuntimeError(msg or f"pdz error {rc}")
+
+
+PLAN_FIELDS = ("kind", "ctas", "ctas_per_strip", "bonus", "geometry", "radius",
+               "partials_per_plane", "strips", "block_rows", "threads", "stop_rule")
+
+
+def plan_info(params) -> dict:
+    """The launch plan of a solve (pdz_solve_plan_info; host only)."""
+    buf = (ctypes.c_int32 * len(PLAN_FIELDS))()
+    check(lib().pdz_solve_plan_info(ctypes.byref(params), buf, len(PLAN_FIELDS)))
+    return dict(zip(PLAN_FIELDS, list(buf)))
+
+
+def kernel_name(params) -> str:
+    """Name of the sweep kernel template a solve launches (pdz_solve_kernel_name)."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib().pdz_solve_kernel_name(ctypes.byref(params), buf, 128))
+    return buf.value.decode()
 
 
 def device():

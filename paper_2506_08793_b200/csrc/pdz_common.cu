@@ -1,4 +1,5 @@
 // Library-wide plumbing: error strings, version, Gaussian taps.
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -21,15 +22,30 @@ int32_t cuda_status(cudaError_t e, const char* where) {
   return PDZ_ECUDA;
 }
 
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev);
+}
+
+// Per device: SM counts differ between device kinds, and a process may drive
+// several GPUs (one thread per device).
 int num_sms() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cached[kMaxDevices] = {};
+  const int dev = current_device();
+  int v = cached[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cached = n > 0 ? n : 148;
+    v = n > 0 ? n : 148;
+    cached[dev].store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
+}
+
+bool first_use_on_device(std::atomic<uint64_t>* mask) {
+  const uint64_t bit = uint64_t(1) << current_device();
+  return (mask->fetch_or(bit) & bit) == 0;
 }
 
 // g = exp(-d^2 / (2 sigma^2)), d = -K/2..K/2, normalised by its sum.  The

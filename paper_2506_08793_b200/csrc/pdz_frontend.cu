@@ -120,12 +120,10 @@ static int32_t rowmin(const double* in, double* out, int H, int W, int r, cudaSt
   }
   const int span = std::min(W, 2048);
   const size_t smem = size_t(2) * (span + 2 * r) * sizeof(double);
-  static bool raised = false;
-  if (!raised) {
+  static std::atomic<uint64_t> raised{0};
+  if (first_use_on_device(&raised))
     cudaFuncSetAttribute(rowmin_vhgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          2 * (2048 + 2 * 2048) * 8);
-    raised = true;
-  }
   rowmin_vhgw_kernel<<<dim3((W + span - 1) / span, H), 256, smem, s>>>(in, out, H, W, r, span);
   PDZ_CHECK_LAUNCH("rowmin");
   return PDZ_OK;

@@ -1,6 +1,7 @@
 // Internal helpers shared by the libpdz translation units (not part of the ABI).
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdarg>
@@ -136,7 +137,14 @@ __host__ __device__ __forceinline__ float f32_from_order_key(uint32_t k) {
 #endif
 }
 
-int num_sms();
+constexpr int kMaxDevices = 64;
+int current_device();  // cudaGetDevice, clamped to [0, kMaxDevices)
+int num_sms();         // SM count of the current device (cached per device)
+// True the first time it is called on the current device for this mask:
+// per-device one-time setup such as cudaFuncSetAttribute (function
+// attributes are per device; a process-wide flag would leave the second GPU
+// of a multi-GPU process at the default 48 KB dynamic shared memory limit).
+bool first_use_on_device(std::atomic<uint64_t>* mask);
 
 // Gaussian 1-D factor in float64 (host).
 int32_t gaussian_taps_host(double sigma, int kernel_size, double* taps);

@@ -549,7 +549,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   SBlock* const q = mb->q;  // generated blocks (at most 3 not done), ring by block number
   int gen = 0, iss = 0, dn = 0;  // blocks generated / issued / done
   int published = 0, fin_seen = 0, granted_k = 0, fin_probe = 0;
-  bool anystop = false;
+  bool anystop = false, aborted = false;
   // open partial: (plane, iteration) of the blocks summed so far
   int acc_p = -1, acc_it = 0, slot_img = -1, slot_k = 0;
   double acc = 0.0;
@@ -602,7 +602,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     PDZ_P(lap(0);)
     // 2. generate the schedule ahead (at most 3 blocks not yet done)
     bool wait_fin = false;
-    while (gen < dn + 3) {
+    while (!aborted && gen < dn + 3) {
       SBlock nb;
       const int k = it.template next<STOP>(a, nb, fin_seen, anystop);
       if (k != kIterBlock) {
@@ -632,7 +632,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     // 3. scan for the next TMA load (block iss): acquire loads of the
     // neighbours' progress, one per lane (the flattened dependency list; an
     // acquire load is a strong load + L1 invalidation, no fence)
-    const bool want = iss < gen && iss < dn + 2;
+    const bool want = !aborted && iss < gen && iss < dn + 2;
     int kpass = 0, need = 0, need_fin = 0;
     int v0 = 0x7fffffff, v1 = 0x7fffffff, vf = 0x7fffffff;
     bool scan = false;
@@ -705,8 +705,10 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     }
     if (wait_fin) fin_probe = __shfl_sync(0xffffffffu, fprobe, 0);
     PDZ_P(lap(5);)
-    // 6. end of the stream: everything done and published
-    if (it.ended && dn == gen && iss == gen && published >= it.completed(a)) {
+    // 6. end of the stream: everything done and published (or, after an
+    // abort, every issued block done: the compute warps then leave cleanly)
+    if ((it.ended && dn == gen && iss == gen && published >= it.completed(a)) ||
+        (aborted && dn == iss)) {
       if (lane == 0) {
         mb->desc[iss & 1].n = 0;
         mbar_arrive(&bars[iss & 1]);  // completes the phase with no bytes
@@ -722,9 +724,14 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       PDZ_P(lap(5);)
       continue;
     }
-    if (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs) {
+    if (!aborted && (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs)) {
+      // a dependency never arrived (or another CTA gave up): flag the abort,
+      // stop generating, let the issued blocks drain and end the stream --
+      // the launch completes, the host raises, the context stays usable
       if (lane == 0) atomicExch(a.flags + 1, 1);
-      __trap();  // a dependency never arrived: fail the launch rather than hang
+      aborted = true;
+      gen = iss;
+      continue;
     }
     PDZ_P(sp[3] += 1; lap(5);)
     __nanosleep(wait_fin || want ? 32 : 64);
@@ -1195,13 +1202,11 @@ template <int R, int V, bool EDGE, bool STOP>
 static StreamFn stream_prepared(size_t* smem) {
   static_assert(SGeo<R, V>::FITS, "staging buffers exceed shared memory");
   static_assert(SGeo<R, V>::ROWS > SGeo<R, V>::SPLIT, "two-part row load");
-  static bool done = false;
+  static std::atomic<uint64_t> done{0};
   *smem = SGeo<R, V>::SMEM;
-  if (!done) {
+  if (first_use_on_device(&done))
     cudaFuncSetAttribute(stream_kernel<R, V, EDGE, STOP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(SGeo<R, V>::SMEM));
-    done = true;
-  }
   return stream_kernel<R, V, EDGE, STOP>;
 }
 

@@ -308,12 +308,10 @@ static size_t tile_smem(int R) {
 
 template <int RT, bool EDGE>
 static SweepFn prepared() {
-  static bool done = false;
-  if (!done) {
+  static std::atomic<uint64_t> done{0};
+  if (first_use_on_device(&done))
     cudaFuncSetAttribute(sweep_kernel<RT, EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(tile_smem(RT >= 0 ? RT : kMaxFusedRadius)));
-    done = true;
-  }
   return sweep_kernel<RT, EDGE>;
 }
 
@@ -933,17 +931,22 @@ static int32_t chunk_graph(const LaunchArgs& la, const pdz_solve_params* p, cons
 // chunk) and stops queueing once every plane has stopped.
 // Measurement hook (pdz_time_sweep_kernels): events around the sweep launches.
 static bool g_time_kernels = false;
-static cudaEvent_t g_kev[2] = {nullptr, nullptr};
-static bool g_kev_recorded = false;
+// Events are per device (an event recorded on another device's stream
+// fails); the last recorded pair is the one pdz_last_sweep_kernel_ms reads.
+static cudaEvent_t g_kev[kMaxDevices][2] = {};
+static int g_kev_dev = -1;
+static std::mutex g_kev_mu;
 
 static void time_mark(int which, cudaStream_t s) {
   if (!g_time_kernels) return;
-  if (!g_kev[0]) {
-    cudaEventCreate(&g_kev[0]);
-    cudaEventCreate(&g_kev[1]);
+  std::lock_guard<std::mutex> lk(g_kev_mu);
+  const int dev = current_device();
+  if (!g_kev[dev][0]) {
+    cudaEventCreate(&g_kev[dev][0]);
+    cudaEventCreate(&g_kev[dev][1]);
   }
-  cudaEventRecord(g_kev[which], s);
-  if (which == 1) g_kev_recorded = true;
+  cudaEventRecord(g_kev[dev][which], s);
+  if (which == 1) g_kev_dev = dev;
 }
 
 static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
@@ -999,10 +1002,14 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   rc = chunk_graph(la, p, pl, s, &exec);
   if (rc != PDZ_OK) return rc;
   const int n_chunks = (p->max_iters + kChunk - 1) / kChunk;
-  static thread_local int32_t* pinned = nullptr;
-  static thread_local cudaEvent_t events[2] = {nullptr, nullptr};
+  // per thread and device: events belong to the device they were created on
+  static thread_local int32_t* pinned_dev[kMaxDevices] = {};
+  static thread_local cudaEvent_t events_dev[kMaxDevices][2] = {};
+  const int dev = current_device();
+  int32_t*& pinned = pinned_dev[dev];
+  cudaEvent_t* events = events_dev[dev];
   if (poll && pinned == nullptr) {
-    PDZ_CUDA(cudaHostAlloc(&pinned, 2 * sizeof(int32_t), cudaHostAllocDefault), "pinned flag");
+    PDZ_CUDA(cudaHostAlloc(&pinned, 2 * sizeof(int32_t), cudaHostAllocPortable), "pinned flag");
     PDZ_CUDA(cudaEventCreateWithFlags(&events[0], cudaEventDisableTiming), "event");
     PDZ_CUDA(cudaEventCreateWithFlags(&events[1], cudaEventDisableTiming), "event");
   }
@@ -1326,10 +1333,16 @@ int32_t pdz_debug_prof(long long* host, int n) {
 void pdz_time_sweep_kernels(int32_t enable) { g_time_kernels = enable != 0; }
 
 float pdz_last_sweep_kernel_ms(void) {
-  if (!g_kev_recorded) return -1.0f;
+  cudaEvent_t e0, e1;
+  {
+    std::lock_guard<std::mutex> lk(g_kev_mu);
+    if (g_kev_dev < 0) return -1.0f;
+    e0 = g_kev[g_kev_dev][0];
+    e1 = g_kev[g_kev_dev][1];
+  }
   float ms = -1.0f;
-  if (cudaEventSynchronize(g_kev[1]) != cudaSuccess) return -1.0f;
-  if (cudaEventElapsedTime(&ms, g_kev[0], g_kev[1]) != cudaSuccess) return -1.0f;
+  if (cudaEventSynchronize(e1) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) return -1.0f;
   return ms;
 }
 
@@ -1337,6 +1350,44 @@ int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params) {
   Plan pl;
   if (check_params(params, &pl) != PDZ_OK) return -1;
   return pl.stream ? 2 : 1;
+}
+
+int32_t pdz_solve_plan_info(const pdz_solve_params* params, int32_t* info_host, int32_t n) {
+  Plan pl;
+  const int32_t rc = check_params(params, &pl);
+  if (rc != PDZ_OK) return rc;
+  const bool rel = params->rel_tol >= 0.0;
+  const int32_t v[PDZ_PLAN_INFO_LEN] = {
+      pl.stream ? 2 : 1,
+      pl.stream ? pl.G : pl.nblk,
+      pl.kps,
+      pl.bonus,
+      pl.geo,
+      pl.R,
+      pl.nbmax,
+      pl.nstrips,
+      pl.stream ? geo_srb(pl.R, pl.geo) : kTH,
+      pl.stream ? geo_threads(pl.geo) : kThreads,
+      rel ? 1 : 0,
+  };
+  for (int i = 0; i < n && i < PDZ_PLAN_INFO_LEN; ++i) info_host[i] = v[i];
+  return PDZ_OK;
+}
+
+int32_t pdz_solve_kernel_name(const pdz_solve_params* params, char* buf_host, int32_t n) {
+  Plan pl;
+  const int32_t rc = check_params(params, &pl);
+  if (rc != PDZ_OK) return rc;
+  if (!buf_host || n <= 0) return PDZ_EINVAL;
+  const int edge = params->edge_preserving ? 1 : 0;
+  if (pl.stream)
+    snprintf(buf_host, size_t(n), "pdz::stream_kernel<%d, %d, %d, %d>", pl.R, pl.geo, edge,
+             params->rel_tol >= 0.0 ? 1 : 0);
+  else
+    snprintf(buf_host, size_t(n), "pdz::sweep_kernel<%d, %d>",
+             (pl.R == 1 || pl.R == 2 || pl.R == 3 || pl.R == 6 || pl.R == 9 || pl.R == 12 ||
+              pl.R == 24) ? pl.R : -1, edge);
+  return PDZ_OK;
 }
 
 }  // extern "C"

@@ -83,12 +83,16 @@ def validate_unit_image(image, defer: bool = False):
                 raise ValueError("image values must lie in [0, 1]")
         return image, check
     # one pinned 3-double slot per thread, read behind an event
-    buf = getattr(_stats_pinned, "buf", None)
+    # (per thread and device: a CUDA event belongs to the device it records on)
+    slots = getattr(_stats_pinned, "slots", None)
+    if slots is None:
+        slots = _stats_pinned.slots = {}
+    buf, ev = slots.get(stats_dev.device.index, (None, None))
     if buf is None:
-        buf = _stats_pinned.buf = torch.empty(3, dtype=torch.float64, pin_memory=True)
-        _stats_pinned.event = torch.cuda.Event()
+        buf = torch.empty(3, dtype=torch.float64, pin_memory=True)
+        ev = torch.cuda.Event()
+        slots[stats_dev.device.index] = (buf, ev)
     buf.copy_(stats_dev, non_blocking=True)
-    ev = _stats_pinned.event
     ev.record()
 
     def deferred_check():

@@ -314,6 +314,19 @@ def dehaze_slabs(image, cfg: SolverConfig | None = None, ablation=(), group=None
                                        _lambda_mode(flags, cfg), with_bounds=True)
     rank, world = ((dist.get_rank(group), dist.get_world_size(group))
                    if dist.is_initialized() else (0, 1))
+    if world == 1:
+        # one rank: the whole-image persistent solve (stop rule on the device,
+        # no blocks, no host round trips) -- bitwise what dehaze() computes
+        from .solver import DeviceProblem, queue_solve_problem
+
+        u, finish = queue_solve_problem(DeviceProblem(phi, lam, h, w, c, c, bounds), cfg,
+                                        edge_preserving="no-edge" not in flags)
+        out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
+        nat.check(nat.lib().pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1,
+                                                 nat.stream_ptr()))
+        traces = finish()
+        return (to_host(out, image),
+                DehazeResult(to_host(a_dev, image), to_host(t_dev, image), traces, flags))
     u_slab, traces = solve_slab(phi, lam, h, cfg, edge_preserving="no-edge" not in flags,
                                 bounds=bounds, group=group)
     u = _all_gather_rows(u_slab.contiguous(), h, group, rank, world)

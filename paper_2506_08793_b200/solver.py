@@ -304,16 +304,20 @@ def queue_solve_problem(problem: DeviceProblem, cfg: SolverConfig, *, edge_prese
                                               ws.numel(), nat.stream_ptr()))
     # one pinned landing buffer per thread: the outcome, then the bounds
     nb_host = nbytes + 8 * P
-    buf = getattr(_solve_pinned, "buf", None)
+    # keyed by device too: a CUDA event belongs to the device it was recorded on
+    slots = getattr(_solve_pinned, "slots", None)
+    if slots is None:
+        slots = _solve_pinned.slots = {}
+    dev_idx = problem.phi.device.index
+    buf, ev = slots.get(dev_idx, (None, None))
     if buf is None or buf.numel() < nb_host:
-        buf = _solve_pinned.buf = torch.empty(max(nb_host, 4096), dtype=torch.uint8,
-                                              pin_memory=True)
-        _solve_pinned.event = torch.cuda.Event()
+        buf = torch.empty(max(nb_host, 4096), dtype=torch.uint8, pin_memory=True)
+        ev = torch.cuda.Event()
+        slots[dev_idx] = (buf, ev)
     buf[:nbytes].copy_(state[:nbytes], non_blocking=True)
     dev_bounds = hasattr(bounds, "is_cuda")
     if dev_bounds:
         buf[nbytes:nb_host].copy_(bounds.contiguous().view(torch.uint8), non_blocking=True)
-    ev = _solve_pinned.event
     ev.record()
 
     def finish():

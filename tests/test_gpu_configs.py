@@ -1,0 +1,220 @@
+"""GPU parity at the BASELINE.json configurations.
+
+Every case runs the CUDA library through the drop-in API and compares it
+with the CPU oracle on the same seeded synthetic inputs:
+
+* config 2 -- 1024^2, K = 19, the full 200 sweeps at full size;
+* config 3 -- a batch of 16 images of 640x480 (K = 13, 100 sweeps) through
+  dehaze_batch: more strip-units than SMs, so the persistent plan splits
+  all strip-rows evenly over the SMs with CTA ranges that span strips AND
+  images (kps == 0, the partial-slot index across images and the covering
+  dependency interval); fixed iterations and a staggered stop rule;
+* config 4 -- 3840x2160, r = 15 front end bit-exact at full size, 5 sweeps
+  at full size, the full 500 sweeps on a 540x3840 crop;
+* config 5 -- 7680x4320, K = 49: front end bit-exact and 3 sweeps at full
+  size, and the tolerance variant (rel_tol 1e-5, max 2000) on a crop with
+  identical iterations_run;
+* dehaze_slabs on one rank.
+
+The solve loop of the oracle runs in C (oracle/pdz_oracle_solve.c, pinned
+to the reference's fixtures by tests/test_oracle_golden.py); the front end
+is the numpy oracle.  Tolerances are the north star's: bit-exact dark
+channel / airlight indices / A / t, max-abs 1e-4 on u, residual norms
+rel 1e-5, identical iterations_run.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import TAU_STABLE
+from oracle import pdz_oracle as orc
+from paper_2506_08793_b200 import synthetic as SYN
+
+pytestmark = pytest.mark.gpu
+
+U_TOL = 1e-4
+NORM_RTOL = 1e-5
+FLAGS = ("no-multiscale", "no-guided")
+
+
+@pytest.fixture(scope="module")
+def pdz():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    import paper_2506_08793_b200 as pkg
+
+    __graft_entry__.build_oracle()
+    pkg._native.lib()
+    orc.native_lib()
+    return pkg
+
+
+def _cfg(pdz, n, **kw):
+    c = SYN.BENCH_CONFIGS[n]
+    base = dict(tau=TAU_STABLE, sigma=c["sigma"], kernel_size=c["kernel_size"],
+                patch_radius=c["patch_radius"], max_iters=c["max_iters"],
+                rel_tol=c.get("rel_tol", 1e-300))
+    base.update(kw)
+    return pdz.SolverConfig(**base)
+
+
+def _check_against_oracle(out, info, img, cfg):
+    ro, ra, rt, rtr = orc.run_pipeline(img, orc.SolverSettings.from_config(cfg), FLAGS,
+                                       native=True)
+    np.testing.assert_array_equal(info.airlight, ra)
+    np.testing.assert_array_equal(info.transmission, rt)
+    err = float(np.max(np.abs(out - ro)))
+    assert err <= U_TOL, err
+    for tr, r in zip(info.traces, rtr):
+        assert tr.iterations_run == r.iterations_run
+        assert tr.converged == r.converged
+        np.testing.assert_allclose(tr.residual_norms, r.residual_norms, rtol=NORM_RTOL)
+    return err
+
+
+def _front_end_bit_exact(pdz, img, radius):
+    from paper_2506_08793_b200 import estimate_atmospheric_light_indices
+    from paper_2506_08793_b200.scattering import dark_channel, estimate_transmission
+
+    dark = dark_channel(img, np.ones(3), radius)
+    np.testing.assert_array_equal(dark, orc.dark_channel(img, np.ones(3), radius))
+    a, picked = estimate_atmospheric_light_indices(img, dark, 0.001)
+    rp = orc.airlight_selection(dark, 0.001)
+    np.testing.assert_array_equal(picked, rp)
+    ra = orc.airlight_from_selection(img, rp)
+    np.testing.assert_array_equal(a, ra)
+    dn = dark_channel(img, a, radius)
+    np.testing.assert_array_equal(dn, orc.dark_channel(img, ra, radius))
+    np.testing.assert_array_equal(estimate_transmission(dn, 0.95),
+                                  orc.transmission_from_dark(dn, 0.95))
+
+
+# ------------------------------------------------------------------ config 2
+
+def test_config2_full_size_all_200_sweeps(pdz):
+    img = SYN.make_hazy_scene(1024, 1024, 2, 0).hazy.astype(np.float64)
+    cfg = _cfg(pdz, 2)
+    out, info = pdz.dehaze(img, cfg, ablation=FLAGS)
+    assert all(tr.iterations_run == 200 for tr in info.traces)
+    _check_against_oracle(out, info, img, cfg)
+
+
+# ------------------------------------------------------------------ config 3
+
+def _c3_batch(pdz, n):
+    return [SYN.make_hazy_scene(480, 640, 3, i).hazy.astype(np.float64)
+            for i in range(n)]
+
+
+def _c3_plan(pdz, batch, cfg):
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import _params
+
+    return nat.plan_info(_params(480, 640, 3 * batch, 3, cfg))
+
+
+@pytest.mark.parametrize("rel_tol", [1e-300, 3e-3])
+def test_config3_batch_plan_spanning_images(pdz, rel_tol):
+    """16 images: 160 strip-units > SMs -> even split of all strip-rows with
+    CTA ranges crossing images (kps == 0).  Every image against the oracle
+    (100 sweeps; with rel_tol = 3e-3 the planes stop between iterations ~60
+    and 100, staggered across images and channels)."""
+    imgs = _c3_batch(pdz, 16)
+    cfg = _cfg(pdz, 3, rel_tol=rel_tol)
+    plan = _c3_plan(pdz, 16, cfg)
+    assert plan["kind"] == 2 and plan["ctas_per_strip"] == 0, plan
+    rows_per_cta = 16 * 10 * 480 / plan["ctas"]
+    assert rows_per_cta % 480 != 0 and plan["partials_per_plane"] >= 2, plan
+    out, res = pdz.dehaze_batch(imgs, cfg, ablation=FLAGS)
+    stops = set()
+    for i, im in enumerate(imgs):
+        _check_against_oracle(out[i], res[i], im, cfg)
+        stops.update(tr.iterations_run for tr in res[i].traces)
+    if rel_tol > 1e-200:
+        assert len(stops) >= 8 and min(stops) < 80, sorted(stops)
+
+
+def test_config3_batch_equals_single_images(pdz):
+    """dehaze_batch on the spanning plan is bitwise the per-image dehaze
+    (norms, iterations_run, u), stop rule armed and staggered."""
+    imgs = _c3_batch(pdz, 16)
+    cfg = _cfg(pdz, 3, rel_tol=3e-3, max_iters=90)
+    out, res = pdz.dehaze_batch(imgs, cfg, ablation=FLAGS)
+    for i in (0, 5, 11, 15):
+        o, r = pdz.dehaze(imgs[i], cfg, ablation=FLAGS)
+        np.testing.assert_array_equal(out[i], o)
+        for x, y in zip(res[i].traces, r.traces):
+            assert x.residual_norms == y.residual_norms
+            assert x.iterations_run == y.iterations_run and x.converged == y.converged
+
+
+# ------------------------------------------------------------------ config 4
+
+@pytest.fixture(scope="module")
+def c4_image(pdz):
+    return SYN.make_hazy_scene(2160, 3840, 4, 0).hazy.astype(np.float64)
+
+
+def test_config4_front_end_bit_exact_full_size(pdz, c4_image):
+    _front_end_bit_exact(pdz, c4_image, 15)
+
+
+def test_config4_full_size_5_sweeps(pdz, c4_image):
+    cfg = _cfg(pdz, 4, max_iters=5)
+    out, info = pdz.dehaze(c4_image, cfg, ablation=FLAGS)
+    _check_against_oracle(out, info, c4_image, cfg)
+
+
+def test_config4_crop_all_500_sweeps(pdz, c4_image):
+    crop = np.ascontiguousarray(c4_image[810:1350])
+    assert crop.shape == (540, 3840, 3)
+    cfg = _cfg(pdz, 4)
+    out, info = pdz.dehaze(crop, cfg, ablation=FLAGS)
+    assert all(tr.iterations_run == 500 for tr in info.traces)
+    _check_against_oracle(out, info, crop, cfg)
+
+
+# ------------------------------------------------------------------ config 5
+
+@pytest.fixture(scope="module")
+def c5_image(pdz):
+    return SYN.make_hazy_scene(4320, 7680, 5, 0).hazy.astype(np.float64)
+
+
+def test_config5_front_end_and_3_sweeps_full_size(pdz, c5_image):
+    _front_end_bit_exact(pdz, c5_image, 7)
+    cfg = _cfg(pdz, 5, max_iters=3, rel_tol=1e-300)
+    out, info = pdz.dehaze(c5_image, cfg, ablation=FLAGS)
+    _check_against_oracle(out, info, c5_image, cfg)
+
+
+@pytest.mark.parametrize("window", [(slice(2000, 2160), slice(3000, 3256)),
+                                    (slice(100, 228), slice(6000, 6384))])
+def test_config5_tolerance_variant_on_a_crop(pdz, c5_image, window):
+    """rel_tol 1e-5, at most 2000 sweeps (the convergence-test variant): the
+    planes stop after ~900-1200 sweeps; iterations_run equal to the oracle's."""
+    crop = np.ascontiguousarray(c5_image[window])
+    cfg = _cfg(pdz, 5)
+    assert cfg.rel_tol == 1e-5 and cfg.max_iters == 2000
+    out, info = pdz.dehaze(crop, cfg, ablation=FLAGS)
+    _check_against_oracle(out, info, crop, cfg)
+
+
+# ---------------------------------------------------------------- row slabs
+
+def test_dehaze_slabs_single_rank(pdz):
+    """dehaze_slabs without a process group (one rank) equals dehaze and the
+    oracle, fixed iterations and stop rule."""
+    from paper_2506_08793_b200.parallel import dehaze_slabs
+
+    img = SYN.make_hazy_scene(300, 512, 4, 1).hazy.astype(np.float64)
+    for cfg in (_cfg(pdz, 4, max_iters=40), _cfg(pdz, 2, max_iters=300, rel_tol=2e-3)):
+        out, info = dehaze_slabs(img, cfg, ablation=FLAGS)
+        o, r = pdz.dehaze(img, cfg, ablation=FLAGS)
+        np.testing.assert_array_equal(out, o)
+        for x, y in zip(info.traces, r.traces):
+            assert x.residual_norms == y.residual_norms
+            assert x.iterations_run == y.iterations_run
+        _check_against_oracle(out, info, img, cfg)

@@ -193,3 +193,29 @@ def test_row_slabs_share_the_global_stop_rule():
         assert [int(p["iters"][c]) for p in parts] == [ref_tr[c].iterations_run] * 2
         assert all(bool(p["conv"][c]) for p in parts)
     np.testing.assert_array_equal(u, ref_u)
+
+
+def _gather_worker(rank, world, port, outdir, height):
+    from paper_2506_08793_b200.parallel import _all_gather_rows
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = torch.arange(3 * height * 5, dtype=torch.float32).reshape(3, height, 5)
+        y0, y1 = slab_bounds(height, world, rank)
+        out = _all_gather_rows(full[:, y0:y1].contiguous(), height, None, rank, world)
+        np.save(os.path.join(outdir, f"g{rank}.npy"), out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,height", [(2, 9), (3, 10), (3, 7)])
+def test_all_gather_rows_over_gloo(world, height):
+    """The final slab gather of dehaze_slabs: ragged last slab (ceil(H/G)
+    rows per rank, remainder on the last), every rank gets the full field."""
+    full = np.arange(3 * height * 5, dtype=np.float32).reshape(3, height, 5)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gather_worker, args=(world, _free_port(), d, height), nprocs=world, join=True)
+        for r in range(world):
+            np.testing.assert_array_equal(np.load(os.path.join(d, f"g{r}.npy")), full)
