@@ -1,27 +1,39 @@
 """Benchmark of the hot path: the relaxed fixed-point dehazing solve.
 
-Workload (BASELINE.json configs[1]): one 1024x1024x3 float32
-synthetic hazy image, patch 15 (r = 7), Gaussian sigma 3 / K = 19, 200
-fixed-point iterations at tau = TAU_STABLE, ablation no-multiscale/no-guided.
-A "step" = one full 200-iteration solve of all 3 channels.
+    python bench.py [--config {1..5}] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-  value  : MPix*it/s of the solve with Phi/lambda already resident in HBM
-           (front end excluded), L2 flushed (256 MiB write) before every step;
-  e2e    : the same metric through the public API `dehaze()` with a pinned
-           host float32 image: H2D copy, front end, solve, clamp and D2H of
-           the float64 result inside the timed region.
+Workloads are the BASELINE.json configs; the default and the
+headline is config 2 (configs[1]): one 1024x1024x3 float32 synthetic hazy
+image, patch 15, sigma 3 / K = 19, 200 fixed-point iterations at
+tau = TAU_STABLE, ablation no-multiscale / no-guided.  A "step" is one full
+solve of the config (all channels, all images of the rank's share).
 
-`python bench.py --gpus N` under torchrun runs one independent image per
-rank (weak scaling, no data-path collective; SURVEY 8(e) batch mode);
-timing is max over ranks.  `--impl reference` times the reference
-algorithm (the CPU oracle port, oracle/pdz_oracle.py) on host cores.
+  value : MPix*it/s of the solve with Phi / lambda already resident in HBM
+          (front end excluded), L2 flushed (256 MiB write) before every step;
+  e2e   : the same metric through the public API (`dehaze`, `dehaze_batch`,
+          `dehaze_slabs`) from pinned host float32 images: H2D copy, front end,
+          solve, clamp and D2H of the float64 result inside the timed region
+          (`e2e_numpy`: the same call with numpy input, as a pdehaze user
+          makes it).
+
+How the configs use N GPUs (one process per GPU under torchrun, max over
+ranks, no fake ranks):
+  config 1, 2 : one independent image per rank (replicas, "weak");
+  config 3    : the 256 images are sharded, ceil(256 / N) per rank, no
+                data-path collective ("strong");
+  config 4, 5 : N = 1 runs the whole-image persistent solve; N > 1 row slabs
+                (paper_2506_08793_b200/parallel.py: halo exchange every k
+                sweeps + one all-reduce of the residual table per block).
+
+`--impl reference` times the reference algorithm (the numpy float64 port of
+the reference's CPU code, oracle/pdz_oracle.py, direct K^2 Gaussian like
+gaussian_convolve) on the host cores, on a bounded sample of the same config.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -33,14 +45,14 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+from paper_2506_08793_b200.synthetic import BENCH_CONFIGS  # noqa: E402
+
 TAU_STABLE = 0.9 * 2.0 / (8.0 / 1e-3 + 0.5)
-H, W, C = 1024, 1024, 3
-K, SIGMA, ITERS, PATCH_R = 19, 3.0, 200, 7
+C = 3
 ABL = ("no-multiscale", "no-guided")
 METRIC = "megapixel-iterations/sec of fixed-point solver"
 UNIT = "MPix*it/s"
 BYTES_PER_PIXEL = (3 * C + 1) * 4  # read u, Phi (C planes), lambda; write u' -> 40 B
-FLOPS_PER_PIXEL = C * (33 + 4 * K)
 
 
 def _env_rank():
@@ -48,15 +60,39 @@ def _env_rank():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
-def _config(extra=None):
-    cfg = {"workload": "config2: 1024x1024x3 f32 synthetic hazy image, patch 15, sigma 3 "
-                       "(K=19), 200 fixed-point iterations, tau=TAU_STABLE",
-           "height": H, "width": W, "channels": C, "kernel_size": K, "sigma": SIGMA,
-           "iterations": ITERS, "tau": TAU_STABLE, "ablation": list(ABL),
-           "l2": "flushed before every timed step (256 MiB memset)"}
-    if extra:
-        cfg.update(extra)
-    return cfg
+def _spec(n: int) -> dict:
+    s = dict(BENCH_CONFIGS[n])
+    s.setdefault("rel_tol", None)  # None: fixed iteration count
+    return s
+
+
+def _workload(n: int) -> dict:
+    """The `config` object: identical in both arms (GPU and --impl reference)."""
+    s = _spec(n)
+    k, h, w, b = s["kernel_size"], s["height"], s["width"], s["batch"]
+    stop = (f"convergence test rel_tol {s['rel_tol']:g}, at most {s['max_iters']} iterations"
+            if s["rel_tol"] else f"{s['max_iters']} fixed-point iterations")
+    return {
+        "workload": f"config{n}: {'%d x ' % b if b > 1 else ''}{w}x{h}x{C} f32 synthetic hazy "
+                    f"image{'s' if b > 1 else ''}, patch {2 * s['patch_radius'] + 1}, sigma "
+                    f"{s['sigma']:g} (K={k}), {stop}, tau=TAU_STABLE",
+        "config_number": n, "height": h, "width": w, "channels": C, "batch": b,
+        "kernel_size": k, "sigma": s["sigma"], "patch_radius": s["patch_radius"],
+        "iterations": s["max_iters"], "rel_tol": s["rel_tol"], "tau": TAU_STABLE,
+        "ablation": list(ABL),
+        "l2": "GPU arm: flushed before every timed step (256 MiB memset); CPU arm: n/a",
+    }
+
+
+def _solver_config(n: int, pdz):
+    s = _spec(n)
+    return pdz.SolverConfig(tau=TAU_STABLE, sigma=s["sigma"], kernel_size=s["kernel_size"],
+                            patch_radius=s["patch_radius"], max_iters=s["max_iters"],
+                            rel_tol=s["rel_tol"] or 1e-300)
+
+
+def _flops_per_pixel(k: int) -> int:
+    return C * (33 + 4 * k)
 
 
 def _peaks():
@@ -67,6 +103,23 @@ def _peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def shard(count: int, world: int, rank: int) -> range:
+    """Images of rank `rank` when `count` images are dealt ceil(count / world) each."""
+    per = -(-count // world)
+    return range(min(count, rank * per), min(count, (rank + 1) * per))
 
 
 class ClockSampler:
@@ -103,7 +156,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.005)  # the timed region is ~35 ms at the default steps
+            time.sleep(0.005)  # the config-2 timed region is ~35 ms at the default steps
 
     def __enter__(self):
         if self._nv is not None:
@@ -124,71 +177,105 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU side
 
-def cpu_solve_sample(iters=2, threads=3):
-    """Reference algorithm (oracle port: direct K^2 Gaussian like
+def cpu_sample_shape(n: int) -> tuple[int, int]:
+    """Rows x columns of the CPU arm's bounded sample: the full image up to
+    config 2, else a crop holding ~1024^2 * 19^2 tap-pixels per iteration (the
+    config-2 cost: ~0.5 s per iteration with 3 channel threads)."""
+    s = _spec(n)
+    budget = 1024 * 1024 * 19 * 19
+    px = max(64 * 64, budget // (s["kernel_size"] ** 2))
+    h, w = s["height"], s["width"]
+    if h * w <= px:
+        return h, w
+    rows = max(2 * s["kernel_size"], min(h, int(px // w)))
+    if rows * w > 2 * px:  # very wide images: crop the columns too
+        w = max(2 * s["kernel_size"], int(2 * px // rows))
+    return rows, w
+
+
+def cpu_solve_sample(n: int, iters: int = 2, threads: int = C):
+    """Reference algorithm (numpy float64 port: direct K^2 Gaussian like
     gaussian_convolve, solver.py:238-240) on the host: `iters` fixed-point
-    iterations of the full 1024^2 config-2 solve, one thread per channel
-    (the reference's `workers` parallelism).  Returns (MPix*it/s, seconds)."""
+    iterations over the sample crop of config n, one thread per channel (the
+    reference's `workers` parallelism).  Returns (MPix*it/s, seconds, (rows, cols))."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import pdz_oracle as orc
     from paper_2506_08793_b200.synthetic import make_hazy_scene
 
-    img = make_hazy_scene(H, W, 2, 0).hazy.astype(np.float64)
-    st = orc.SolverSettings(tau=TAU_STABLE, sigma=SIGMA, kernel_size=K, patch_radius=PATCH_R,
-                            max_iters=iters, rel_tol=1e-300)
-    dark = orc.dark_channel(img, np.ones(C), PATCH_R)
+    s = _spec(n)
+    rows, cols = cpu_sample_shape(n)
+    img = make_hazy_scene(rows, cols, n, 0).hazy.astype(np.float64)
+    st = orc.SolverSettings(tau=TAU_STABLE, sigma=s["sigma"], kernel_size=s["kernel_size"],
+                            patch_radius=s["patch_radius"], max_iters=iters, rel_tol=1e-300)
+    dark = orc.dark_channel(img, np.ones(C), st.patch_radius)
     a = orc.airlight_from_selection(img, orc.airlight_selection(dark, st.airlight_fraction))
-    t = orc.transmission_from_dark(orc.dark_channel(img, a, PATCH_R), st.omega)
+    t = orc.transmission_from_dark(orc.dark_channel(img, a, st.patch_radius), st.omega)
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as pool:
         list(pool.map(lambda c: orc.relaxed_solve(img[:, :, c], t, float(a[c]), st),
                       range(C)))
     dt = time.perf_counter() - t0
-    return H * W * iters / dt / 1e6, dt
+    return rows * cols * iters / dt / 1e6, dt, (rows, cols)
 
 
-def cpu_front_end_seconds():
+def cpu_front_end_seconds(n: int) -> float:
     from oracle import pdz_oracle as orc
     from paper_2506_08793_b200.synthetic import make_hazy_scene
 
-    img = make_hazy_scene(H, W, 2, 0).hazy.astype(np.float64)
+    s = _spec(n)
+    rows, cols = cpu_sample_shape(n)
+    img = make_hazy_scene(rows, cols, n, 0).hazy.astype(np.float64)
+    r = s["patch_radius"]
     t0 = time.perf_counter()
-    dark = orc.dark_channel(img, np.ones(C), PATCH_R)
+    dark = orc.dark_channel(img, np.ones(C), r)
     a = orc.airlight_from_selection(img, orc.airlight_selection(dark, 0.001))
-    t = orc.transmission_from_dark(orc.dark_channel(img, a, PATCH_R), 0.95)
+    t = orc.transmission_from_dark(orc.dark_channel(img, a, r), 0.95)
     (img - a * (1.0 - t)[:, :, None]) / np.maximum(t, 0.1)[:, :, None]
     orc.haze_weight(t)
     return time.perf_counter() - t0
+
+
+def _cpu_baseline(n: int, value, dt, shape, iters, extra=""):
+    s = _spec(n)
+    return {"value": value, "unit": UNIT, "cores": C, "kind": "port",
+            "sample": f"oracle port of the reference (numpy float64, direct K^2 Gaussian as in "
+                      f"the reference), {iters} iterations of the K={s['kernel_size']} solve on "
+                      f"a {shape[0]}x{shape[1]} {'crop' if shape != (s['height'], s['width']) else 'image'}"
+                      f" of config {n}, {C} channel threads, {dt:.1f} s{extra}",
+            "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()}
 
 
 def run_reference(args):
     rank, _, world = _env_rank()
     if rank != 0:
         return 0
-    fe = cpu_front_end_seconds()
-    for _ in range(args.warmup):
-        pass  # the CPU port has no JIT/cache state worth warming beyond imports
-    samples = []
+    n = args.config
+    s = _spec(n)
+    fe = cpu_front_end_seconds(n)
     iters = 2
+    samples, shape = [], None
     for _ in range(args.steps):
-        _, dt = cpu_solve_sample(iters=iters)
+        _, dt, shape = cpu_solve_sample(n, iters=iters)
         samples.append(dt)
     per_iter = statistics.mean(samples) / iters
-    total = fe + ITERS * per_iter  # extrapolated full config-2 run
-    value = H * W * ITERS / total / 1e6
+    # per-pixel cost of the sample scaled to the config: front end once per
+    # image, then the config's iteration count (extrapolated, labelled)
+    scale = s["height"] * s["width"] * s["batch"] / (shape[0] * shape[1])
+    total = (fe + s["max_iters"] * per_iter) * scale
+    value = s["height"] * s["width"] * s["batch"] * s["max_iters"] / total / 1e6
+    base = _cpu_baseline(n, value, statistics.mean(samples), shape, iters,
+                         f" per step x {args.steps} steps, front end once ({fe:.2f} s); "
+                         f"extrapolated to {s['max_iters']} iterations"
+                         + (f" and {scale:.1f}x the pixels" if scale != 1.0 else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config({"parallelism": "host threads (channels)"}),
-        "cpu_baseline": {
-            "value": value, "unit": UNIT, "cores": C, "kind": "port",
-            "sample": f"oracle port of the reference (numpy float64, direct K^2 Gaussian), "
-                      f"front end once ({fe:.2f} s) + {iters} solve iterations per step x "
-                      f"{args.steps} steps at 1024^2, 3 channel threads; extrapolated to "
-                      f"{ITERS} iterations",
-            "host_cpus": os.cpu_count()},
+        "data": "synthetic (seeded generator of SURVEY 8(d); no public dataset)",
+        "config": _workload(n), "parallelism": f"host threads: {C} (one per channel)",
+        "extrapolated": True, "timed_iterations": iters * args.steps,
+        "timed_seconds": sum(samples), "cpu_baseline": base,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -196,6 +283,17 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU side
+
+def _mode(n: int, world: int) -> tuple[str, str]:
+    """(how the config uses the ranks, weak | strong)."""
+    b = _spec(n)["batch"]
+    if b > 1:
+        return f"batch shards: ceil({b} / {world}) images per GPU, no collective", "strong"
+    if n >= 4 and world > 1:
+        return (f"row slabs x{world}: halo exchange every k sweeps + residual all-reduce "
+                f"(NCCL)"), "strong"
+    return f"replicas x{world} (one image per GPU)", "weak"
+
 
 def run_gpu(args):
     import torch
@@ -210,45 +308,101 @@ def run_gpu(args):
 
     import paper_2506_08793_b200 as pdz
     from paper_2506_08793_b200 import _native as nat
-    from paper_2506_08793_b200.solver import (DeviceProblem, _front_end, _image_dev,
-                                              _lambda_mode, _params, prepare_problem)
+    from paper_2506_08793_b200 import parallel as par
+    from paper_2506_08793_b200.solver import (_front_end, _image_dev, _lambda_mode, _params,
+                                              prepare_problem)
     from paper_2506_08793_b200.synthetic import make_hazy_scene
 
+    n = args.config
+    s = _spec(n)
+    h, w, batch, iters = s["height"], s["width"], s["batch"], s["max_iters"]
+    tol = s["rel_tol"]
     lib = nat.lib()
-    cfg = pdz.SolverConfig(tau=TAU_STABLE, sigma=SIGMA, kernel_size=K, patch_radius=PATCH_R,
-                           max_iters=ITERS, rel_tol=1e-300)
-    scene = make_hazy_scene(H, W, 2, rank)
-    host_img = torch.from_numpy(scene.hazy).pin_memory()
-
-    # device-resident solver inputs (outside the timed region)
-    img_dev, is_f64 = _image_dev(host_img)
+    cfg = _solver_config(n, pdz)
     flags = frozenset(ABL)
-    t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
-    phi, lam = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg))
-    prob = DeviceProblem(phi, lam, H, W, C, C)
-    prm = _params(H, W, C, C, cfg)
-    ws = torch.empty(lib.pdz_solve_workspace_bytes(prm), dtype=torch.uint8, device=phi.device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=phi.device)
+    slabs = n >= 4 and batch == 1 and world > 1
+    how, scaling = _mode(n, world)
+
+    # ---- this rank's images (host, pinned) and device-resident solver inputs
+    if batch > 1:
+        mine = list(shard(batch, world, rank))
+    elif slabs:
+        mine = [0]  # every rank holds the one image
+    else:
+        mine = [rank]  # replicas: a different seed per rank
+    host = [torch.from_numpy(make_hazy_scene(h, w, n, i).hazy).pin_memory() for i in mine]
+    nimg = len(host)
+    dev = torch.device("cuda", local)
+    phi = torch.empty((max(nimg, 1) * C, h, w), dtype=torch.float32, device=dev)
+    lam = torch.empty((max(nimg, 1), h, w), dtype=torch.float32, device=dev)
+    for i, img in enumerate(host):
+        img_dev, is_f64 = _image_dev(img)
+        t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
+        prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
+                        phi=phi[C * i:C * i + C], lam=lam[i])
+        del img_dev, t_dev, a_dev
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    planes = nimg * C
+    prm = _params(h, w, max(planes, C), C, cfg)
+    # pixel-iterations one step of this rank performs (the tolerance variant
+    # reads its iteration counts back after each solve)
+    px_iters = [float(nimg * h * w * iters)]
 
-    def solve():
-        nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(prob.phi), nat.ptr(prob.lam),
-                                                   nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+    if slabs:
+        # device-resident slab solve: Phi / lambda of the rank's extended slab
+        def solve():
+            solver = par.SlabSolver(phi, lam[0], h, cfg, tau=cfg.tau, rank=rank, world=world)
+            _, _, its, _ = solver.solve(cfg.max_iters, cfg.rel_tol)
+            px_iters[0] = h * w * sum(its) / len(its) / world  # this rank's share
+        kernel_timed = False
+    elif nimg == 0:
+        def solve():
+            pass
+        kernel_timed = False
+    elif tol:
+        ws = torch.empty(lib.pdz_solve_workspace_bytes(prm), dtype=torch.uint8, device=dev)
+        nstate = int(lib.pdz_solve_state_bytes(prm))
+        state = torch.empty(nstate, dtype=torch.uint8, device=dev)
+        u_out = torch.empty_like(phi)
+        pin = torch.empty(nstate, dtype=torch.uint8, pin_memory=True)
 
-    for _ in range(max(args.warmup, 3)):
-        flush.zero_()
-        solve()
-    torch.cuda.synchronize()
+        def solve():
+            nat.check(lib.pdz_fixed_point_solve_async(prm, nat.ptr(phi), nat.ptr(lam),
+                                                      nat.ptr(u_out), nat.ptr(state),
+                                                      nat.ptr(ws), ws.numel(), nat.stream_ptr()))
+            pin.copy_(state, non_blocking=True)
+        kernel_timed = True
+    else:
+        ws = torch.empty(lib.pdz_solve_workspace_bytes(prm), dtype=torch.uint8, device=dev)
+
+        def solve():
+            nat.check(lib.pdz_fixed_point_sweeps_async(prm, nat.ptr(phi), nat.ptr(lam),
+                                                       nat.ptr(ws), ws.numel(),
+                                                       nat.stream_ptr()))
+        kernel_timed = True
+
+    def read_iterations():
+        if not tol or slabs or nimg == 0:
+            return
+        torch.cuda.synchronize()
+        ints = pin.numpy()[8 * iters * planes:].view(np.int32)
+        px_iters[0] = float(h * w * ints[:planes].sum()) / C
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        solve()
+    torch.cuda.synchronize()
+    read_iterations()
+
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kernel_ms = []  # the persistent sweep kernel alone (library events on its stream)
-    lib.pdz_time_sweep_kernels(1)
+    lib.pdz_time_sweep_kernels(1 if kernel_timed else 0)
     with ClockSampler(local) as clocks:
         barrier()
         for i in range(args.steps):
@@ -258,95 +412,119 @@ def run_gpu(args):
             ends[i].record(stream)
         barrier()
     lib.pdz_time_sweep_kernels(0)
-    kernel_ms.append(float(lib.pdz_last_sweep_kernel_ms()))
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    launch_ms = float(lib.pdz_last_sweep_kernel_ms()) if kernel_timed else -1.0
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     ms = statistics.mean(step_ms)
-    if dist is not None:
-        t = torch.tensor([ms], device=phi.device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * H * W * ITERS / (ms / 1e3) / 1e6
+    read_iterations()
+
+    def over_ranks(x, op):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    ms = over_ranks(ms, dist.ReduceOp.MAX if dist else None)
+    work = over_ranks(px_iters[0], dist.ReduceOp.SUM if dist else None)  # whole job
+    value = work / (ms / 1e3) / 1e6
 
     # roofline of the dominant kernel: the persistent sweep kernel, ONE launch
-    # per solve (all 200 sweeps).  achieved = algorithmic bytes per launch
-    # (40 B/px/sweep x H x W x 200) / the launch's device time,
-    # read from CUDA events the library records around that launch on its
-    # stream (pdz_time_sweep_kernels); the last timed step's launch.
+    # per solve (every sweep).  achieved = algorithmic bytes per launch (40 B
+    # per RGB pixel per sweep, x the pixel-iterations the launch
+    # ran) / the launch's device time, read from CUDA events the library
+    # records around that launch on its stream (the last timed step's launch).
     peak, peak_src = _peaks()
-    kind = int(lib.pdz_sweep_kernel_kind(prm))
-    launch_ms = kernel_ms[-1] if kernel_ms and kernel_ms[-1] > 0 else ms
-    if dist is not None:
-        t = torch.tensor([launch_ms], device=phi.device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        launch_ms = float(t.item())
-    alg_bytes = BYTES_PER_PIXEL * H * W * ITERS
+    if launch_ms <= 0:
+        launch_ms = ms
+    launch_ms = over_ranks(launch_ms, dist.ReduceOp.MAX if dist else None)
+    alg_bytes = BYTES_PER_PIXEL * px_iters[0]  # per launch = this rank's solve
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(REPO, "profiles", "sweep_ncu_summary.json")
-    if os.path.exists(prof):
+    if n == 2 and os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
+    plan = nat.plan_info(prm) if planes else {}
+    kname = nat.kernel_name(prm) if planes else ""
+    sweeps = px_iters[0] / max(1, nimg * h * w)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
-                "fp32_tflops": FLOPS_PER_PIXEL * H * W * ITERS / (launch_ms / 1e3) / 1e12,
-                "kernel": ("pdz::stream_kernel<9,true> (persistent, 200 sweeps per launch)"
-                           if kind == 2 else "pdz::sweep_kernel<9,true> (tiled, 1 sweep per launch)"),
+                "fp32_tflops": _flops_per_pixel(s["kernel_size"]) * px_iters[0]
+                / (launch_ms / 1e3) / 1e12,
+                "kernel": f"{kname} ({'persistent, every sweep of the solve in one launch' if plan.get('kind') == 2 else 'tiled, 1 sweep per launch'})"
+                          + (" per k-sweep block of a slab" if slabs else ""),
                 "launch_ms": launch_ms, "share_of_step": launch_ms / ms,
-                "us_per_sweep": launch_ms * 1e3 / ITERS}
+                "us_per_sweep": launch_ms * 1e3 / max(sweeps, 1e-9), "plan": plan}
 
-    # e2e through the public API: pinned host image -> dehaze -> host result.
-    # A CPU-tensor input returns a CPU float64 tensor (numpy in -> numpy out,
-    # like the reference), so the device->host read is inside the call.
-    def e2e_step():
-        out, _ = pdz.dehaze(host_img, cfg, ablation=ABL)
-        assert out.device.type == "cpu" and out.dtype == torch.float64
+    # ---- e2e through the public API: pinned host images -> result on the host
+    def api_call(images):
+        if batch > 1:
+            if not images:
+                return None
+            out, res = pdz.dehaze_batch(images, cfg, ablation=ABL)
+            return res[0].traces
+        if slabs:
+            _, res = par.dehaze_slabs(images[0], cfg, ablation=ABL)
+            return res.traces
+        out, res = pdz.dehaze(images[0], cfg, ablation=ABL)
+        return res.traces
 
-    for _ in range(2):
-        e2e_step()
-    torch.cuda.synchronize()
-    e_ms = []
-    for _ in range(max(3, min(args.steps, 10))):
-        flush.zero_()
+    def time_api(images, reps):
+        api_call(images)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms.append(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
-    e2e_ms = statistics.mean(e_ms)
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device=phi.device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    # host reads per step: the restored image (H, W, C) f64, the transmission
-    # map (H, W) f64 and the airlight (C,) f64 of DehazeResult
-    e2e = {"value": world * H * W * ITERS / (e2e_ms / 1e3) / 1e6, "unit": UNIT,
-           "h2d_bytes_per_step": H * W * C * 4,
-           "d2h_bytes_per_step": H * W * C * 8 + H * W * 8 + C * 8,
-           "ms_per_step": e2e_ms}
+        out_ms, its = [], None
+        for _ in range(reps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            traces = api_call(images)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            out_ms.append(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
+            if traces is not None and tol:
+                its = sum(t.iterations_run for t in traces) / len(traces)
+        return over_ranks(statistics.mean(out_ms), dist.ReduceOp.MAX if dist else None), its
+
+    # the long configs take seconds per call: fewer repetitions
+    reps = max(1, min(args.steps, 10 if ms < 50 else 3 if ms < 500 else 1))
+    e2e_ms, its = time_api(host, reps)
+    e2e_work = work if its is None else over_ranks(
+        float(h * w * its) * (1.0 / world if slabs else 1.0), dist.ReduceOp.SUM if dist else None)
+    # host traffic per step and rank: images in (f32); restored image (f64),
+    # transmission map and airlight (f64) of DehazeResult out
+    e2e = {"value": e2e_work / (e2e_ms / 1e3) / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": nimg * h * w * C * 4,
+           "d2h_bytes_per_step": nimg * (h * w * C * 8 + h * w * 8 + C * 8),
+           "ms_per_step": e2e_ms, "input": "pinned host float32 torch tensors", "reps": reps}
+    e2e_numpy = None
+    if world == 1 and h * w * batch <= 1 << 23:  # numpy in / numpy out like a pdehaze user
+        np_ms, np_its = time_api([t.numpy() for t in host], reps)
+        np_work = work if np_its is None else float(h * w * np_its)
+        e2e_numpy = {"value": np_work / (np_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": np_ms,
+                     "input": "pageable numpy float32 arrays (numpy in, numpy float64 out)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt = cpu_solve_sample(iters=2)
-        cpu = {"value": v, "unit": UNIT, "cores": C, "kind": "port",
-               "sample": f"oracle port (numpy float64, direct K^2 Gaussian as in the "
-                         f"reference) 2 iterations of the 1024^2 K=19 solve, 3 channel "
-                         f"threads, {dt:.1f} s, front end excluded like `value`",
-               "host_cpus": os.cpu_count()}
+        v, dt, shape = cpu_solve_sample(n, iters=2)
+        cpu = _cpu_baseline(n, v, dt, shape, 2, ", front end excluded like `value`")
 
     if rank == 0:
+        launches = int(lib.pdz_solve_kernel_launches(prm)) if kernel_timed else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator of SURVEY 8(d); no public dataset)",
-            "config": _config({"parallelism": f"replicas x{world} (one image per GPU)"}),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(lib.pdz_solve_kernel_launches(prm)) * args.steps,
+            "config": _workload(n), "parallelism": how,
+            "per_gpu": {"value": value / world, "unit": UNIT, "hbm_frac": achieved / peak},
+            "sweeps_per_step": sweeps,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_numpy": e2e_numpy,
+            "gpu_launches": (launches * args.steps) if launches is not None else
+            "per k-sweep block: 1 persistent launch + pad/extract copies (slab mode)",
             "clocks": clocks.summary(),
             "step_ms": step_ms,
         }
@@ -362,6 +540,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(BENCH_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -279,8 +279,10 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 template <bool EDGE>
 __device__ __forceinline__ float sflux(float jump, float along, float eps) {
   if (!EDGE) return jump;
-  const float s = fmaf(jump, jump, along * along);
-  return jump * rcp_approx(sqrt_approx(s) + eps);
+  // explicit roundings: no fma contraction with the caller's adds, so every
+  // kernel instantiation (block geometry, border variant) rounds alike
+  const float s = fmaf(jump, jump, __fmul_rn(along, along));
+  return __fmul_rn(jump, rcp_approx(__fadd_rn(sqrt_approx(s), eps)));
 }
 
 // Packed float pairs (FADD2 / FMUL2): per-lane IEEE round-to-nearest, so a
@@ -313,6 +315,19 @@ __device__ __forceinline__ float2 sflux2(float2 jump, float2 along, float2 eps2)
   const float2 s = ffma2(jump, jump, mul2(along, along));
   const float2 q = add2(make_float2(sqrt_approx(s.x), sqrt_approx(s.y)), eps2);
   return mul2(jump, make_float2(rcp_approx(q.x), rcp_approx(q.y)));
+}
+
+// 1 / (|(jump, along)| + eps) per lane (1 when !EDGE): the coefficient of a
+// face whose flux enters the divergence as an explicit fused multiply-add
+// (ptxas otherwise contracts the packed product with the add or sub that
+// follows in SOME unrolled rows only, and a pixel's rounding would depend on
+// its row's position in the warp's row group, i.e. on the launch plan).
+template <bool EDGE>
+__device__ __forceinline__ float2 sflux2_coef(float2 jump, float2 along, float2 eps2) {
+  if (!EDGE) return make_float2(1.f, 1.f);
+  const float2 s = ffma2(jump, jump, mul2(along, along));
+  const float2 q = add2(make_float2(sqrt_approx(s.x), sqrt_approx(s.y)), eps2);
+  return make_float2(rcp_approx(q.x), rcp_approx(q.y));
 }
 
 // ----------------------------------------------------------- iteration --
@@ -959,9 +974,14 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
     // Item -> (row i, column group g): 8 consecutive items = 8 consecutive rows
     // of one group (a conflict-free quarter-warp, see SGeo).
     const int hitems = ((hn + 7) & ~7) * (kSTW / 8);
-    for (int item = tid; item < hitems; item += kComputeThreads) {
-      const int i = (item >> 6) * 8 + (item & 7), g = (item >> 3) & 7;
-      if (i >= hn) continue;
+    constexpr int OFF = Gm::RP - R;
+    constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
+    // staged values of one item -> registers (false: no such item)
+    auto hfetch = [&](int item, float (&v)[4 * NQ], int& i, int& g) -> bool {
+      if (item >= hitems) return false;
+      i = (item >> 6) * 8 + (item & 7);
+      g = (item >> 3) & 7;
+      if (i >= hn) return false;
       const int y = ylo + i;  // a pad row reads its mirror source row
       const int si = (y < 0 ? -1 - y : (y >= H ? 2 * H - 1 - y : y)) - ylo;
       if (!got2 && si >= kSplit) {
@@ -969,9 +989,6 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
         got2 = true;
       }
       const float* row = in_cur + si * Gm::PITCH + 8 * g;
-      constexpr int OFF = Gm::RP - R;
-      constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
-      float v[4 * NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const float4 t = reinterpret_cast<const float4*>(row)[q];
@@ -980,6 +997,9 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
         v[4 * q + 2] = t.z;
         v[4 * q + 3] = t.w;
       }
+      return true;
+    };
+    auto hcompute = [&](float (&v)[4 * NQ], int i, int g) {
       // pad columns in registers, compile-time indices per group: left
       // (staged column 8g + t < RP) <- 2 RP - 1 - 8g - t, in the groups that
       // reach it (8g + OFF < RP, i.e. g < R / 8); right (full last strip,
@@ -1037,6 +1057,11 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
       float4* dst = reinterpret_cast<float4*>(h_cur + i * Gm::HP + 8 * g);
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
       dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+    };
+    for (int item = tid; item < hitems; item += kComputeThreads) {
+      float v[4 * NQ];
+      int i, g;
+      if (hfetch(item, v, i, g)) hcompute(v, i, g);
     }
     if (!got2) mbar_wait(&bars[5 + ib], par);  // the vertical pass reads every row
     PDZ_P({ const long long t = clock64(); pf[2] += t - tq; tq = t; })
@@ -1110,8 +1135,9 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
         }
         float2 xA = make_float2(cA.y - eA.x, eA.y - cA.x);  // raw centred x-differences
         float2 xB = make_float2(cB.y - eB.x, eB.y - cB.x);
-        // south flux of the row above the first output row
-        float2 fs_up = sflux2<EDGE>(sub2(cB, cA), mul2(hx2, add2(xA, xB)), eps2);
+        // south face of the row above the first output row: jump and coefficient
+        float2 ju = sub2(cB, cA);
+        float2 ru = sflux2_coef<EDGE>(ju, mul2(hx2, add2(xA, xB)), eps2);
 #pragma unroll
         for (int j = 0; j < kRPW; ++j) {
           urow += Gm::PITCH;
@@ -1132,13 +1158,17 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
           // negated, (u0 - l, u1 - r) = cB - eB; sflux is odd in the jump, so
           // the pair is (fw, -fe) exactly
           const float2 fwe = sflux2<EDGE>(sub2(cB, eB), mul2(hy2, add2(de, d)), eps2);
-          const float fm = sflux<EDGE>(u1 - u0, hy * (d.x + d.y), a.eps);  // face c|c+1
-          const float2 fs_dn = sflux2<EDGE>(sub2(cC, cB), mul2(hx2, add2(xB, xC)), eps2);
+          const float fm = sflux<EDGE>(__fsub_rn(u1, u0), __fmul_rn(hy, __fadd_rn(d.x, d.y)), a.eps);  // face c|c+1
+          const float2 jd = sub2(cC, cB);
+          const float2 rd = sflux2_coef<EDGE>(jd, mul2(hx2, add2(xB, xC)), eps2);
           // div0 = ((fm - fw) + s0) - n0, div1 = ((fe - fm) + s1) - n1, with
-          // fe - fm = -(fm + (-fe)) exactly
-          const float2 div = sub2(add2(make_float2(fm - fwe.x, -(fm + fwe.y)), fs_dn), fs_up);
+          // fe - fm = -(fm + (-fe)) exactly; the south and north fluxes
+          // s = jd * rd, n = ju * ru enter as fused multiply-adds
+          const float2 we = make_float2(__fsub_rn(fm, fwe.x), -__fadd_rn(fm, fwe.y));
+          const float2 div = ffma2(make_float2(-ju.x, -ju.y), ru, ffma2(jd, rd, we));
           const float2 cB_old = cB;
-          fs_up = fs_dn;
+          ju = jd;
+          ru = rd;
           eA = eB;
           cA = cB;
           xA = xB;
@@ -1213,6 +1243,9 @@ static StreamFn stream_prepared(size_t* smem) {
 template <int V, bool EDGE, bool STOP>
 static StreamFn stream_pick_radius(int R, size_t* smem) {
   switch (R) {  // radii whose staging fits in shared memory (SGeo<R, V>::FITS)
+#ifdef PDZ_ONLY_R  // experiment builds (tools/): one radius, a minute to compile
+    case PDZ_ONLY_R: return stream_prepared<PDZ_ONLY_R, PDZ_ONLY_R == 24 ? 0 : V, EDGE, STOP>(smem);
+#else
     case 1: return stream_prepared<1, V, EDGE, STOP>(smem);
     case 2: return stream_prepared<2, V, EDGE, STOP>(smem);
     case 3: return stream_prepared<3, V, EDGE, STOP>(smem);
@@ -1220,6 +1253,7 @@ static StreamFn stream_pick_radius(int R, size_t* smem) {
     case 9: return stream_prepared<9, V, EDGE, STOP>(smem);
     case 12: return stream_prepared<12, V, EDGE, STOP>(smem);
     case 24: return V == 0 ? stream_prepared<24, 0, EDGE, STOP>(smem) : nullptr;
+#endif
     default: return nullptr;
   }
 }

@@ -10,6 +10,8 @@ samples are copied back.
 
 from __future__ import annotations
 
+import re
+
 import numpy as np
 
 from . import _native as nat
@@ -17,38 +19,42 @@ from .image import is_device_array, to_device, validate_image
 
 __all__ = ["NetpbmError", "load_image", "save_image"]
 
-_WHITESPACE = (b" ", b"\t", b"\n", b"\r", b"\x0b", b"\x0c")
+_GAP = re.compile(rb"(?:[ \t\n\r\x0b\x0c]|#[^\n]*)*")   # whitespace and `#` comments
+_WORD = re.compile(rb"[^ \t\n\r\x0b\x0c#]+")
+_SPACE = b" \t\n\r\x0b\x0c"
+_FORMATS = {b"P5": 1, b"P6": 3}  # magic -> channels
 
 
 class NetpbmError(ValueError):
     """Malformed or unsupported Netpbm file (image.py:30-31)."""
 
 
-def _token(raw: bytes, pos: int):
-    """Next header token after whitespace and `#` comments (to end of line)."""
-    n = len(raw)
-    while pos < n:
-        ch = raw[pos:pos + 1]
-        if ch == b"#":
-            nl = raw.find(b"\n", pos)
-            pos = n if nl < 0 else nl
-        elif ch in _WHITESPACE:
-            pos += 1
-        else:
-            break
-    start = pos
-    while pos < n and raw[pos:pos + 1] not in _WHITESPACE and raw[pos:pos + 1] != b"#":
-        pos += 1
-    if pos == start:
-        raise NetpbmError("malformed header: unexpected end of header")
-    return raw[start:pos], pos
+class _Header:
+    """Cursor over the header bytes: words separated by whitespace / comments."""
 
+    def __init__(self, raw: bytes, start: int):
+        self.raw = raw
+        self.pos = start
 
-def _int_field(raw: bytes, pos: int, what: str):
-    tok, pos = _token(raw, pos)
-    if not tok.isdigit():
-        raise NetpbmError(f"malformed header: expected integer {what}, got {tok!r}")
-    return int(tok), pos
+    def word(self) -> bytes:
+        self.pos = _GAP.match(self.raw, self.pos).end()
+        found = _WORD.match(self.raw, self.pos)
+        if found is None:
+            raise NetpbmError("malformed header: unexpected end of header")
+        self.pos = found.end()
+        return found.group()
+
+    def number(self, what: str) -> int:
+        text = self.word()
+        if not text.isdigit():
+            raise NetpbmError(f"malformed header: expected integer {what}, got {text!r}")
+        return int(text)
+
+    def end(self) -> int:
+        """Offset of the payload: exactly one whitespace byte closes the header."""
+        if self.pos >= len(self.raw) or self.raw[self.pos] not in _SPACE:
+            raise NetpbmError("malformed header: missing whitespace after maxval")
+        return self.pos + 1
 
 
 def load_image(path) -> np.ndarray:
@@ -56,27 +62,22 @@ def load_image(path) -> np.ndarray:
     header comments tolerated (image.py:91-125)."""
     with open(path, "rb") as fh:
         raw = fh.read()
-    magic = raw[:2]
-    if magic not in (b"P5", b"P6"):
+    channels = _FORMATS.get(raw[:2])
+    if channels is None:
         raise NetpbmError(
-            f"malformed header: not a binary Netpbm (P5/P6) file, magic {magic!r}")
-    channels = 1 if magic == b"P5" else 3
-    width, pos = _int_field(raw, 2, "width")
-    height, pos = _int_field(raw, pos, "height")
-    maxval, pos = _int_field(raw, pos, "maxval")
-    if width < 1 or height < 1:
+            f"malformed header: not a binary Netpbm (P5/P6) file, magic {raw[:2]!r}")
+    header = _Header(raw, 2)
+    width, height, maxval = (header.number(n) for n in ("width", "height", "maxval"))
+    if min(width, height) < 1:
         raise NetpbmError(f"malformed header: non-positive dimensions {width}x{height}")
     if maxval != 255:
         raise NetpbmError(f"unsupported maxval {maxval}: only 255 is supported")
-    if pos >= len(raw) or raw[pos:pos + 1] not in _WHITESPACE:
-        raise NetpbmError("malformed header: missing whitespace after maxval")
-    pos += 1  # one whitespace byte ends the header
-    count = width * height * channels
-    payload = raw[pos:pos + count]
-    if len(payload) < count:
-        raise NetpbmError(f"truncated payload: expected {count} bytes, found {len(payload)}")
-    samples = np.frombuffer(payload, dtype=np.uint8).astype(np.float64) / 255.0
-    return samples.reshape(height, width, channels)
+    start = header.end()
+    want = width * height * channels
+    samples = np.frombuffer(raw, dtype=np.uint8, count=min(want, len(raw) - start), offset=start)
+    if samples.size < want:
+        raise NetpbmError(f"truncated payload: expected {want} bytes, found {samples.size}")
+    return (samples.astype(np.float64) / 255.0).reshape(height, width, channels)
 
 
 def quantize(image):
