@@ -255,6 +255,30 @@ int32_t pdz_fixed_point_sweeps_from(const pdz_solve_params* params, const float*
                                     int32_t count_hi, float* u_out, double* sumsq,
                                     int32_t* failed, void* workspace, size_t workspace_bytes,
                                     void* stream);
+/* The same block with the iterates RESIDENT in the workspace between calls
+ * (the production engine of row-slab mode): nothing is copied into or out of
+ * the padded iterate layout per block.  pdz_slab_layout reports where the
+ * nbuf iterate buffers live inside a workspace of
+ * pdz_solve_workspace_bytes(params): info_host[0..8) <- {nbuf, byte offset
+ * of buffer 0, 1, 2 (-1: absent), pad rows, pad columns, padded rows per
+ * plane, padded row pitch in floats}; buffer b holds float32
+ * [P][H + 2 pad_rows][W + 2 pad_cols] with the field at [pad_rows, pad_cols).
+ * The offsets do not depend on params->max_iters, so one workspace sized for
+ * the largest block serves every block.  pdz_fixed_point_sweeps_resident
+ * runs params->max_iters sweeps starting from buffer `base`: when u_init is
+ * non-NULL (the first block) that buffer is first filled from u_init
+ * (device [P][H][W]) and every buffer's pads are poisoned; otherwise the
+ * buffer's field is taken as it is -- the caller has written the k*R halo
+ * rows it received straight into it (the rest is the previous block's
+ * result).  The final iterate is left in buffer (base + max_iters) % nbuf.
+ * sumsq / failed as in pdz_fixed_point_sweeps_from.  Asynchronous. */
+#define PDZ_SLAB_LAYOUT_LEN 8
+int32_t pdz_slab_layout(const pdz_solve_params* params, int64_t* info_host, int32_t n);
+int32_t pdz_fixed_point_sweeps_resident(const pdz_solve_params* params, const float* u_init,
+                                        const float* phi, const float* lambda_map,
+                                        int32_t count_lo, int32_t count_hi, int32_t base,
+                                        double* sumsq, int32_t* failed, void* workspace,
+                                        size_t workspace_bytes, void* stream);
 /* Number of kernels pdz_fixed_point_sweeps_async launches for `params`
  * (benchmark bookkeeping). */
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params);

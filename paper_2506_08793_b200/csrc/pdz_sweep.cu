@@ -964,26 +964,38 @@ static int32_t queue_extract(const pdz_solve_params* p, const Plan& pl, const So
 
 // u_init: the first iterate (nullptr: u0 = Phi, solver.py:333); rows
 // [cnt_lo, cnt_hi) are the ones counted in the norms.
+// resident_base >= 0 (row-slab blocks, pdz_fixed_point_sweeps_resident): the
+// iterate buffers stay in the workspace between calls; the sweeps start from
+// buffer `resident_base` (filled from u_init only when that is given), the
+// final iterate stays in buffer (resident_base + max_iters) % nbuf and no
+// dense copy is made.
 static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const SolveLayout& L,
                            const float* phi, const float* lam, float* out, cudaStream_t s,
                            bool poll, const float* u_init = nullptr, int cnt_lo = 0,
-                           int cnt_hi = -1) {
+                           int cnt_hi = -1, int resident_base = -1) {
   LaunchArgs la;
-  int32_t rc = fill_args(p, pl, L.buf0, L.buf1, L.buf2, phi, lam, L.psum, L.pflag, L.st, L.sy,
+  float* bufs[3] = {L.buf0, L.buf1, L.buf2};
+  const int nbuf = pl.stream ? kNBuf : 2;
+  const bool resident = resident_base >= 0;
+  if (resident) {
+    float* all[3] = {L.buf0, L.buf1, L.buf2};
+    for (int i = 0; i < nbuf; ++i) bufs[i] = all[(resident_base + i) % nbuf];
+  }
+  int32_t rc = fill_args(p, pl, bufs[0], bufs[1], bufs[2], phi, lam, L.psum, L.pflag, L.st, L.sy,
                          &la);
   if (rc != PDZ_OK) return rc;
   if (cnt_hi < 0) cnt_hi = p->height;
   la.tile.cnt_lo = la.stream.cnt_lo = cnt_lo;
   la.tile.cnt_hi = la.stream.cnt_hi = cnt_hi;
-  if (u_init == nullptr) u_init = phi;
-  {
+  if (u_init == nullptr && !resident) u_init = phi;
+  if (u_init != nullptr) {
     const int64_t rows = int64_t(p->planes) * (p->height + 2 * pl.pad_r);
     const int blocks = int(std::min<int64_t>(rows, int64_t(num_sms()) * 16));
     const int vec = p->width % 4 == 0 && pl.pad_c % 4 == 0 && aligned16(u_init) &&
                     aligned16(L.buf0) && aligned16(L.buf1) && (!L.buf2 || aligned16(L.buf2));
-    pad_init_kernel<<<blocks, 256, 0, s>>>(u_init, L.buf0, pl.stream ? L.buf1 : nullptr, L.buf2,
-                                           p->height, p->width, p->planes, pl.pad_r, pl.pad_c,
-                                           vec);
+    pad_init_kernel<<<blocks, 256, 0, s>>>(u_init, bufs[0], pl.stream ? bufs[1] : nullptr,
+                                           pl.stream ? bufs[2] : nullptr, p->height, p->width,
+                                           p->planes, pl.pad_r, pl.pad_c, vec);
     PDZ_CHECK_LAUNCH("u0 = Phi");
   }
   init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
@@ -995,7 +1007,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
     rc = launch_stream(la, pl, s);
     time_mark(1, s);
     if (rc != PDZ_OK) return rc;
-    return queue_extract(p, pl, L, out, s);
+    return resident ? PDZ_OK : queue_extract(p, pl, L, out, s);
   }
 
   cudaGraphExec_t exec;
@@ -1045,7 +1057,7 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
   PDZ_CUDA(cudaLaunchKernelEx(&cfg, finalize_kernel, L.st, pt, int(p->planes), launched,
                               int(p->max_iters), p->rel_tol),
            "finalize launch");
-  return queue_extract(p, pl, L, out, s);
+  return resident ? PDZ_OK : queue_extract(p, pl, L, out, s);
 }
 
 static int32_t check_abort(const Plan& pl, const Sync& sy) {
@@ -1292,6 +1304,60 @@ int32_t pdz_fixed_point_sweeps_from(const pdz_solve_params* params, const float*
   }
   cudaStream_t s = as_stream(stream);
   rc = queue_solve(&fixed, pl, L, phi, lambda_map, u_out, s, false, u_init, count_lo, count_hi);
+  if (rc != PDZ_OK) return rc;
+  const size_t P = params->planes;
+  PDZ_CUDA(cudaMemcpyAsync(sumsq, L.st.sums, size_t(params->max_iters) * P * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s),
+           "sums copy");
+  PDZ_CUDA(cudaMemcpyAsync(failed, L.st.failed, P * sizeof(int32_t), cudaMemcpyDeviceToDevice, s),
+           "failed copy");
+  return PDZ_OK;
+}
+
+int32_t pdz_slab_layout(const pdz_solve_params* params, int64_t* info_host, int32_t n) {
+  Plan pl;
+  int32_t rc = check_params(params, &pl);
+  if (rc != PDZ_OK) return rc;
+  PDZ_REQUIRE(info_host && n >= PDZ_SLAB_LAYOUT_LEN, "info buffer too small");
+  pdz_solve_params fixed = *params;
+  fixed.rel_tol = -1.0;
+  SolveLayout L = carve_solve(&fixed, pl, reinterpret_cast<void*>(uintptr_t(256)), ~size_t(0) >> 1);
+  const auto off = [&](const float* q) {
+    return q ? int64_t(reinterpret_cast<uintptr_t>(q) - uintptr_t(256)) : int64_t(-1);
+  };
+  info_host[0] = pl.stream ? kNBuf : 2;
+  info_host[1] = off(L.buf0);
+  info_host[2] = off(L.buf1);
+  info_host[3] = off(L.buf2);
+  info_host[4] = pl.pad_r;
+  info_host[5] = pl.pad_c;
+  info_host[6] = int64_t(params->height) + 2 * pl.pad_r;
+  info_host[7] = int64_t(params->width) + 2 * pl.pad_c;
+  return PDZ_OK;
+}
+
+int32_t pdz_fixed_point_sweeps_resident(const pdz_solve_params* params, const float* u_init,
+                                        const float* phi, const float* lambda_map,
+                                        int32_t count_lo, int32_t count_hi, int32_t base,
+                                        double* sumsq, int32_t* failed, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  Plan pl;
+  int32_t rc = solve_plan(params, phi, lambda_map, &pl);
+  if (rc != PDZ_OK) return rc;
+  PDZ_REQUIRE(phi && lambda_map && sumsq && failed, "NULL array argument");
+  PDZ_REQUIRE(base >= 0 && base < (pl.stream ? kNBuf : 2), "base buffer %d out of range", base);
+  PDZ_REQUIRE(0 <= count_lo && count_lo < count_hi && count_hi <= params->height,
+              "count window [%d, %d) outside the %d rows", count_lo, count_hi, params->height);
+  pdz_solve_params fixed = *params;
+  fixed.rel_tol = -1.0;  // exactly max_iters sweeps: the caller applies the stop rule
+  SolveLayout L = carve_solve(&fixed, pl, workspace, workspace_bytes);
+  if (workspace == nullptr || L.bytes > workspace_bytes) {
+    set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
+    return PDZ_EWORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  rc = queue_solve(&fixed, pl, L, phi, lambda_map, nullptr, s, false, u_init, count_lo, count_hi,
+                   base);
   if (rc != PDZ_OK) return rc;
   const size_t P = params->planes;
   PDZ_CUDA(cudaMemcpyAsync(sumsq, L.st.sums, size_t(params->max_iters) * P * sizeof(double),
