@@ -528,3 +528,64 @@ def test_partial_strip_repeats_bitwise(pdz, shape, k, reps):
         u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg)
         assert np.array_equal(u, u0)
         assert tr.residual_norms == tr0.residual_norms
+
+
+# compute-sanitizer is closed on this pool (profiles/r2_sanitizer_closed.txt), so
+# out-of-bounds writes are looked for with guard bands instead: every buffer a
+# solve touches (Phi, lambda, the result, the state block and the workspace
+# with the padded iterates, partial rings and sync words) sits inside ONE
+# allocation between 64 KiB bands of a byte pattern; whatever the kernels write
+# outside their buffers lands in a band.
+@pytest.mark.parametrize("h,w,k,planes,channels,iters,tol", [
+    (96, 136, 13, 3, 3, 5, 1e-300),     # partial last strip, persistent kernel
+    (120, 128, 49, 3, 3, 3, 1e-300),    # R = 24 geometry
+    (300, 64, 13, 6, 3, 4, 1e-300),     # two images, several blocks per pass
+    (80, 128, 7, 3, 3, 200, 1e-3),      # stop rule: finaliser, frozen planes
+    (33, 65, 19, 2, 1, 4, 1e-300),      # odd width: tiled kernel
+    (2, 2, 5, 1, 1, 3, 1e-300),         # smallest field
+])
+def test_guard_bands_untouched(pdz, h, w, k, planes, channels, iters, tol):
+    import torch
+
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import _params
+
+    lib = nat.lib()
+    cfg = pdz.SolverConfig(tau=TAU_STABLE, kernel_size=k, sigma=max(1.0, k / 6.0),
+                           max_iters=iters, rel_tol=tol)
+    prm = _params(h, w, planes, channels, cfg)
+    rng = np.random.default_rng(h * w + k)
+    phi = rng.uniform(0.0, 1.0, (planes, h, w)).astype(np.float32)
+    lam = rng.uniform(0.05, 0.5, (planes // channels, h, w)).astype(np.float32)
+    sizes = [phi.nbytes, lam.nbytes, phi.nbytes, int(lib.pdz_solve_state_bytes(prm)),
+             int(lib.pdz_solve_workspace_bytes(prm))]
+    band, fill = 64 << 10, 0xA5
+    offs, pos = [], band
+    for n in sizes:
+        offs.append(pos)
+        pos += (n + 255) // 256 * 256 + band
+    arena = torch.full((pos,), fill, dtype=torch.uint8, device="cuda")
+    view = [arena[o:o + n] for o, n in zip(offs, sizes)]
+    view[0].copy_(torch.from_numpy(phi.view(np.uint8).reshape(-1)))
+    view[1].copy_(torch.from_numpy(lam.view(np.uint8).reshape(-1)))
+    for _ in range(2):  # the second solve reuses the workspace as the first left it
+        nat.check(lib.pdz_fixed_point_solve_async(prm, nat.ptr(view[0]), nat.ptr(view[1]),
+                                                  nat.ptr(view[2]), nat.ptr(view[3]),
+                                                  nat.ptr(view[4]), sizes[4], nat.stream_ptr()))
+    torch.cuda.synchronize()
+    inside = torch.zeros(pos, dtype=torch.bool, device="cuda")
+    for o, n in zip(offs, sizes):
+        inside[o:o + n] = True
+    assert bool((arena[~inside] == fill).all()), "a kernel wrote outside its buffers"
+    assert bool((view[0].cpu() == torch.from_numpy(phi.view(np.uint8).reshape(-1))).all())
+    assert bool((view[1].cpu() == torch.from_numpy(lam.view(np.uint8).reshape(-1))).all())
+    u = view[2].cpu().numpy().view(np.float32).reshape(planes, h, w)
+    assert np.isfinite(u).all()
+    if tol < 1e-200:  # fixed sweep count: the last plane against the oracle
+        st = orc.SolverSettings.from_config(cfg)
+        p = planes - 1
+        src, lm = phi[p].astype(np.float64), lam[p // channels].astype(np.float64)
+        ru = src
+        for _ in range(iters):
+            ru, _ = orc.relaxed_step(ru, src, lm, st, separable=True)
+        assert np.max(np.abs(u[p] - ru)) <= U_TOL
