@@ -1249,14 +1249,30 @@ static StreamFn stream_pick_radius(int R, size_t* smem) {
     case 1: return stream_prepared<1, V, EDGE, STOP>(smem);
     case 2: return stream_prepared<2, V, EDGE, STOP>(smem);
     case 3: return stream_prepared<3, V, EDGE, STOP>(smem);
+    case 4: return stream_prepared<4, V, EDGE, STOP>(smem);
     case 6: return stream_prepared<6, V, EDGE, STOP>(smem);
     case 9: return stream_prepared<9, V, EDGE, STOP>(smem);
     case 12: return stream_prepared<12, V, EDGE, STOP>(smem);
+    case 16: return V == 0 ? stream_prepared<16, 0, EDGE, STOP>(smem) : nullptr;
+    case 20: return V == 0 ? stream_prepared<20, 0, EDGE, STOP>(smem) : nullptr;
     case 24: return V == 0 ? stream_prepared<24, 0, EDGE, STOP>(smem) : nullptr;
 #endif
     default: return nullptr;
   }
 }
+// Smallest compiled radius >= R (0: none).  Keep in step with
+// stream_pick_radius.
+static int stream_compiled_radius(int R) {
+#ifdef PDZ_ONLY_R
+  return R <= PDZ_ONLY_R ? PDZ_ONLY_R : 0;
+#else
+  static const int kCompiled[] = {1, 2, 3, 4, 6, 9, 12, 16, 20, 24};
+  for (int r : kCompiled)
+    if (r >= R) return r;
+  return 0;
+#endif
+}
+
 template <bool EDGE>
 static StreamFn stream_pick(int R, int V, bool stop, size_t* smem) {
   if (V == 0)

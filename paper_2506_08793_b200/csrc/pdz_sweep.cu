@@ -264,8 +264,16 @@ __global__ void chunk_base_kernel(StateView st) {
   pdl_launch_dependents();
 }
 
-__global__ void init_state_kernel(StateView st, int P) {
+// Solve state and (G > 0: the persistent kernel) its progress counters.
+__global__ void init_state_kernel(StateView st, int P, int32_t* done = nullptr,
+                                  int32_t* fin = nullptr, int32_t* flags = nullptr, int G = 0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < G) done[p] = 0;
+  if (p == 0 && G > 0) {
+    fin[0] = 0;
+    flags[0] = 0;
+    flags[1] = 0;
+  }
   if (p < P) {
     st.stop_iter[p] = 0;
     st.converged[p] = 0;
@@ -334,7 +342,8 @@ static SweepFn pick_kernel(int R) {
 // fallback as graph-replayed per-sweep launches.
 struct Plan {
   bool stream = false;
-  int R = 1;
+  int R = 1;       // radius the kernel runs (persistent: a compiled radius >= R_taps)
+  int R_taps = 1;  // K / 2 of the Gaussian (>= 1)
   int tiles_x = 0, tiles_y = 0, nblk = 0;  // tiled
   int G = 0, nstrips = 0;                   // streaming
   int kps = 0, bonus = 0;                   // per-strip partition (Partials)
@@ -404,18 +413,26 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
     g_force_tiled = (e && e[0] == '1') ? 1 : 0;
   }
   Plan& P = *pl;
-  P.R = std::max(1, p->kernel_size / 2);
+  P.R = P.R_taps = std::max(1, p->kernel_size / 2);
   const bool edge = p->edge_preserving != 0;
   size_t smem = 0;
   StreamFn sfn = nullptr;
   const int64_t images = p->planes / p->channels;
   const int64_t strip_rows = int64_t((p->width + kSTW - 1) / kSTW) * p->height * images;
-  const int rp = (P.R + 3) & ~3;
-  if (allow_stream && !g_force_tiled && p->width % 4 == 0 && p->height >= 2 * P.R &&
+  // The persistent kernel is compiled for a set of radii; any other odd K
+  // runs on the next compiled radius with its taps centred between zeros
+  // (a zero tap times a finite staged value adds an exact 0, and the border
+  // reflection of the wider kernel only feeds zero taps), so every K <= 49
+  // takes the fast path (solver.py:225-241 accepts any odd K).
+  const int rc = stream_compiled_radius(P.R);
+  const int rp = (rc + 3) & ~3;
+  if (allow_stream && !g_force_tiled && rc > 0 && p->width % 4 == 0 && p->height >= 2 * rc &&
       p->width >= 2 * rp &&
-      strip_rows + p->height < (int64_t(1) << 31))
-    sfn = edge ? stream_pick<true>(P.R, 0, p->rel_tol >= 0.0, &smem)
-               : stream_pick<false>(P.R, 0, p->rel_tol >= 0.0, &smem);
+      strip_rows + p->height < (int64_t(1) << 31)) {
+    sfn = edge ? stream_pick<true>(rc, 0, p->rel_tol >= 0.0, &smem)
+               : stream_pick<false>(rc, 0, p->rel_tol >= 0.0, &smem);
+    if (sfn) P.R = rc;
+  }
   int occ = 0;
   if (sfn) {
     const cudaError_t e =
@@ -430,6 +447,7 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
               fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
     }
   }
+  if (!(sfn && int64_t(num_sms()) * occ >= 2)) P.R = P.R_taps;  // tiled kernel: the true radius
   if (sfn && int64_t(num_sms()) * occ >= 2) {
     P.stream = true;
     P.pad_r = P.R;
@@ -621,11 +639,10 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   if (rc != PDZ_OK) return rc;
   float w[kMaxTaps] = {0.f};
   const int K = p->kernel_size;
-  if (K == 1) {  // identity smoothing expressed as taps (0, 1, 0), R = 1
-    w[1] = float(taps[0]);
-  } else {
-    for (int i = 0; i < K; ++i) w[i] = float(taps[i]);
-  }
+  // taps centred in the kernel radius actually run (pl.R >= K / 2: zeros on
+  // both sides; K = 1 is the identity expressed as (0, 1, 0) at R = 1)
+  const int shift = pl.R - K / 2;
+  for (int i = 0; i < K; ++i) w[i + shift] = float(taps[i]);
   Partials pt;
   pt.sum = psum;
   pt.flag = pflag;
@@ -744,16 +761,6 @@ static int32_t launch_stream(const LaunchArgs& la, const Plan& pl, cudaStream_t 
   PDZ_CUDA(cudaLaunchKernelEx(&cfg, reinterpret_cast<StreamFn>(pl.fn), la.stream),
            "persistent sweep launch");
   return PDZ_OK;
-}
-
-__global__ void sync_init_kernel(Sync sy, int G) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G; i += gridDim.x * blockDim.x)
-    sy.done[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sy.fin[0] = 0;
-    sy.flags[0] = 0;
-    sy.flags[1] = 0;
-  }
 }
 
 // u0 = Phi into a (possibly padded) iterate buffer.  The persistent kernel's
@@ -998,17 +1005,18 @@ static int32_t queue_solve(const pdz_solve_params* p, const Plan& pl, const Solv
                                            p->planes, pl.pad_r, pl.pad_c, vec);
     PDZ_CHECK_LAUNCH("u0 = Phi");
   }
-  init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
-  PDZ_CHECK_LAUNCH("init state");
   if (pl.stream) {
-    sync_init_kernel<<<(pl.G + 255) / 256, 256, 0, s>>>(L.sy, pl.G);
-    PDZ_CHECK_LAUNCH("sync init");
+    init_state_kernel<<<(std::max<int>(p->planes, pl.G) + 255) / 256, 256, 0, s>>>(
+        L.st, p->planes, L.sy.done, L.sy.fin, L.sy.flags, pl.G);
+    PDZ_CHECK_LAUNCH("init state");
     time_mark(0, s);
     rc = launch_stream(la, pl, s);
     time_mark(1, s);
     if (rc != PDZ_OK) return rc;
     return resident ? PDZ_OK : queue_extract(p, pl, L, out, s);
   }
+  init_state_kernel<<<(p->planes + 255) / 256, 256, 0, s>>>(L.st, p->planes);
+  PDZ_CHECK_LAUNCH("init state");
 
   cudaGraphExec_t exec;
   rc = chunk_graph(la, p, pl, s, &exec);
@@ -1355,23 +1363,18 @@ int32_t pdz_fixed_point_sweeps_resident(const pdz_solve_params* params, const fl
     set_error("workspace too small: need %zu bytes, got %zu", L.bytes, workspace_bytes);
     return PDZ_EWORKSPACE;
   }
-  cudaStream_t s = as_stream(stream);
-  rc = queue_solve(&fixed, pl, L, phi, lambda_map, nullptr, s, false, u_init, count_lo, count_hi,
-                   base);
-  if (rc != PDZ_OK) return rc;
-  const size_t P = params->planes;
-  PDZ_CUDA(cudaMemcpyAsync(sumsq, L.st.sums, size_t(params->max_iters) * P * sizeof(double),
-                           cudaMemcpyDeviceToDevice, s),
-           "sums copy");
-  PDZ_CUDA(cudaMemcpyAsync(failed, L.st.failed, P * sizeof(int32_t), cudaMemcpyDeviceToDevice, s),
-           "failed copy");
-  return PDZ_OK;
+  // the finaliser writes the per-sweep sums and the failure record straight
+  // into the caller's buffers (same layouts as the state block's)
+  L.st.sums = sumsq;
+  L.st.failed = failed;
+  return queue_solve(&fixed, pl, L, phi, lambda_map, nullptr, as_stream(stream), false, u_init,
+                     count_lo, count_hi, base);
 }
 
 int64_t pdz_solve_kernel_launches(const pdz_solve_params* params) {
   Plan pl;
   if (check_params(params, &pl) != PDZ_OK) return -1;
-  if (pl.stream) return 5;  // pad init + init state + sync init + persistent + extract
+  if (pl.stream) return 4;  // pad init + init state + persistent + extract
   const int64_t chunks = (params->max_iters + kChunk - 1) / kChunk;
   return 4 + chunks * (1 + kChunk);  // pad init + init + chunk prologues + sweeps + finalize + extract
 }

@@ -589,3 +589,25 @@ def test_guard_bands_untouched(pdz, h, w, k, planes, channels, iters, tol):
         for _ in range(iters):
             ru, _ = orc.relaxed_step(ru, src, lm, st, separable=True)
         assert np.max(np.abs(u[p] - ru)) <= U_TOL
+
+
+@pytest.mark.parametrize("k", [9, 11, 15, 17, 21, 23, 27, 31, 37, 41, 47])
+def test_every_odd_kernel_size_takes_the_persistent_kernel(pdz, k):
+    """The reference accepts any odd K (solver.py:225-241).  Radii that are
+    not compiled run on the next compiled radius with zero taps around the
+    Gaussian: same plan kind (2 = persistent) and the oracle's answer."""
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import _params
+
+    shape = (160, 192)
+    rng = np.random.default_rng(k)
+    ch = rng.random(shape) * 0.8 + 0.1
+    t = 0.3 + 0.6 * rng.random(shape)
+    cfg = pdz.SolverConfig(tau=TAU_STABLE, kernel_size=k, sigma=k / 6.0, max_iters=6,
+                           rel_tol=1e-300)
+    plan = nat.plan_info(_params(shape[0], shape[1], 1, 1, cfg))
+    assert plan["kind"] == 2 and plan["radius"] >= k // 2, plan
+    u, tr = pdz.fixed_point_solve(ch, t, 0.9, cfg)
+    ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg), separable=True)
+    assert np.max(np.abs(u - ru)) <= U_TOL
+    np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
