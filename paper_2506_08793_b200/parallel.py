@@ -192,7 +192,7 @@ class _ResidentEngine:
 # persistent launch plus two small init launches, and an exchange costs two
 # NCCL point-to-point launches plus its bytes at the NVLink peer-copy rate.
 _SWEEP_TFLOPS = 26.0
-_BLOCK_LAUNCH_US = 12.0
+_BLOCK_LAUNCH_US = 26.0  # ~7 us of launches around + ~19 us pipeline fill / drain inside
 _EXCHANGE_LATENCY_US = 20.0
 _NVLINK_BYTES_PER_US = 770e3
 

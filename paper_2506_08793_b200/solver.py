@@ -521,8 +521,14 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
 def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
     """Extension for batched serving (BASELINE config 3): same results as
     calling `dehaze` on each image, but every image's planes are swept by one
-    launch per iteration.  `images`: (B, H, W, C) array or sequence of equal-
-    shaped images.  Returns (restored (B, H, W, C), [DehazeResult] * B)."""
+    persistent launch.  `images`: (B, H, W, C) array or sequence of equal-
+    shaped images.  Returns (restored (B, H, W, C), [DehazeResult] * B).
+
+    The batch is uploaded into one device tensor and validated there with one
+    deferred reduction (finite, min, max over the whole batch); the per-image
+    front ends, the solve, the clamp and the result copies are all queued
+    before the host reads anything back, and the transmission maps and
+    airlights travel to the host as two stacked copies while the solve runs."""
     import torch
 
     cfg = cfg or SolverConfig()
@@ -530,41 +536,73 @@ def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
     if "no-pde" in flags:
         outs = [dehaze(im, cfg, ablation) for im in images]
         return np.stack([o for o, _ in outs]), [r for _, r in outs]
-    batch = [validate_image(im) for im in images]
-    if not batch:
+    items = list(images)
+    if not items:
         raise ValueError("images must be nonempty")
-    shape = tuple(batch[0].shape)
-    if any(tuple(b.shape) != shape for b in batch):
+    shape = tuple(items[0].shape)
+    if len(shape) != 3 or shape[2] not in (1, 3):
+        raise ValueError(f"expected (H, W, C) image with C in {{1, 3}}, got shape {shape}")
+    if any(tuple(im.shape) != shape for im in items):
         raise ValueError("all images of a batch must share one shape")
     h, w, c = shape
     if h < 2 or w < 2:
         raise ValueError(f"field must be at least 2x2, got {(h, w)}")
-    B = len(batch)
+    B = len(items)
     dev = nat.device()
+    like = items[0]
+    # float32 inputs stay float32 on the device (like dehaze); anything else
+    # is carried in float64
+    def kind(im):
+        return str(im.dtype).replace("torch.", "")
+
+    dtype = torch.float32 if all(kind(im) == "float32" for im in items) else torch.float64
+    stack = torch.empty((B, h, w, c), dtype=dtype, device=dev)
+    # uploads run on a side stream in groups of 16 images; the front ends of
+    # a group start as soon as its copies landed (copy engine || SMs)
+    main = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(main)
+    landed = []
+    with torch.cuda.stream(side):
+        for i, im in enumerate(items):
+            src = im if is_device_array(im) else torch.from_numpy(np.ascontiguousarray(im))
+            stack[i].copy_(src, non_blocking=True)
+            if i % 16 == 15 or i == B - 1:
+                ev = torch.cuda.Event()
+                ev.record(side)
+                landed.append(ev)
+    stack.record_stream(side)
+    is_f64 = 1 if dtype == torch.float64 else 0
     phi = torch.empty((B * c, h, w), dtype=torch.float32, device=dev)
     lam = torch.empty((B, h, w), dtype=torch.float32, device=dev)
-    fronts, bounds = [], []
-    for i, im in enumerate(batch):
-        _unit_range(im)
-        img_dev, is_f64 = _image_dev(im)
-        t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
-        _, _, b = prepare_problem(img_dev, is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
+    ts, airs, bounds = [], [], []
+    for i in range(B):
+        if i % 16 == 0:
+            main.wait_event(landed[i // 16])
+        t_dev, a_dev = _front_end(stack[i], is_f64, cfg, flags)
+        _, _, b = prepare_problem(stack[i], is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
                                   phi=phi[i * c:(i + 1) * c], lam=lam[i], with_bounds=True)
-        fronts.append((t_dev, a_dev))
+        ts.append(t_dev)
+        airs.append(a_dev)
         bounds.append(b)
+    _, unit_check = validate_unit_image(stack.view(B * h, w, c), defer=True)
+    t_all, a_all = torch.stack(ts), torch.stack(airs)
+    del ts, airs
+    t_host, a_host = to_host_async(t_all, like), to_host_async(a_all, like)
     problem = DeviceProblem(phi, lam, h, w, B * c, c, torch.cat(bounds))
-    u, traces = solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
     lib = nat.lib()
     for i in range(B):
         nat.check(lib.pdz_clamp_interleave(nat.ptr(u[i * c:(i + 1) * c]), h, w, c,
                                            nat.ptr(out[i]), 1, nat.stream_ptr()))
-    like = images[0] if isinstance(images, (list, tuple)) else images
-    results = []
-    for i, (t_dev, a_dev) in enumerate(fronts):
-        results.append(DehazeResult(to_host(a_dev, like), to_host(t_dev, like),
-                                    traces[i * c:(i + 1) * c], flags))
-    return to_host(out, like), results
+    out_host = to_host_async(out, like)
+    unit_check()  # the errors of a bad batch come before any result
+    traces = finish()
+    t_res, a_res = t_host(), a_host()
+    results = [DehazeResult(a_res[i], t_res[i], traces[i * c:(i + 1) * c], flags)
+               for i in range(B)]
+    return out_host(), results
 
 
 def write_trace_csv(traces, path) -> None:
