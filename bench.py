@@ -440,7 +440,7 @@ def run_gpu(args):
     alg_bytes = BYTES_PER_PIXEL * px_iters[0]  # per launch = this rank's solve
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
-    prof = os.path.join(REPO, "profiles", "sweep_ncu_summary.json")
+    prof = os.path.join(REPO, "profiles", "r2_sweep_ncu_summary.json")
     if n == 2 and os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
