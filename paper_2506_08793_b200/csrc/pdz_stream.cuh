@@ -334,6 +334,7 @@ __device__ __forceinline__ float2 sflux2_coef(float2 jump, float2 along, float2 
 struct SBlock {
   int p, x0, yb, n;  // plane, strip origin, first row, rows
   int iter, c;       // pass (iter, c)
+  int img;           // image of the plane (p / C)
 };
 
 // One pass over the CTA's range [L0, L1) of strip-rows: (image b, strip s,
@@ -379,6 +380,7 @@ struct RangeIter {
         }
       }
       blk.p = p;
+      blk.img = b;
       blk.x0 = s * kSTW;
       blk.yb = y;
       blk.n = min(a.srb, seg_end - L);
@@ -566,36 +568,40 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   int published = 0, fin_seen = 0, granted_k = 0, fin_probe = 0;
   bool anystop = false, aborted = false;
   // open partial: (plane, iteration) of the blocks summed so far
-  int acc_p = -1, acc_it = 0, slot_img = -1, slot_k = 0;
+  int acc_p = -1, acc_it = 0, acc_img = 0, slot_img = -1, slot_k = 0;
   double acc = 0.0;
   int acc_nf = 0;
+  static_assert((kRing & (kRing - 1)) == 0, "ring slots by mask");
   auto flush = [&]() {
     if (acc_p < 0) return;
     if (lane == 0) {
-      const int img = acc_p / C;
-      if (img != slot_img) {  // the CTA's index within the image's range
-        slot_img = img;
-        slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(img) * a.pt.U));
+      if (acc_img != slot_img) {  // the CTA's index within the image's range
+        slot_img = acc_img;
+        slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(acc_img) * a.pt.U));
       }
-      const size_t slot = (size_t(acc_it % a.pt.ring) * a.P + acc_p) * a.pt.nbmax + slot_k;
+      const size_t slot = (size_t(acc_it & (kRing - 1)) * a.P + acc_p) * a.pt.nbmax + slot_k;
       a.pt.sum[slot] = acc;
       a.pt.flag[slot] = acc_nf;
     }
     acc_p = -1;
   };
   long long t0 = global_ns();
+  int idle = 0;
   // [0] rounds [1] dependency-scan cycles [2] publications [3] sleeps
   // [4] done events [5] cycles from a block's IN issue to its done being seen
   PDZ_P(long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long t_iss[4] = {0, 0, 0, 0}; int want_k = 0;)
-  PDZ_P(long long tr = clock64(); long long rp[6] = {0, 0, 0, 0, 0, 0};)
-  // rp: cycles in [0] done events [1] generation [2] scan [3] grant + TMA
-  // [4] sleeping [5] publication + rest
+  PDZ_P(long long tr = clock64(); long long rp[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
+  // rp: cycles in [0] done tests [1] generation [2] scan [3] grant + TMA
+  // [4] sleeping [5] rest [6] r^2 reduction of done blocks [7] the release store
   while (true) {
     bool progressed = false;
     PDZ_P(sp[0] += 1;)
     PDZ_P(auto lap = [&](int i) { const long long t = clock64(); rp[i] += t - tr; tr = t; };)
     // 1. blocks the compute warps finished (in order)
-    while (dn < iss && mbar_test(&bars[3 + (dn & 1)], uint32_t((dn >> 1) & 1))) {
+    while (true) {
+      const bool fin_blk = dn < iss && mbar_test(&bars[3 + (dn & 1)], uint32_t((dn >> 1) & 1));
+      PDZ_P(lap(0);)
+      if (!fin_blk) break;
       const SBlock& b = q[dn & 3];
       // lane w holds warp w's value; a fixed butterfly sums them (lane 0's
       // result is the one stored: deterministic)
@@ -605,6 +611,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         flush();
         acc_p = b.p;
         acc_it = b.iter;
+        acc_img = b.img;
         acc = 0.0;
         acc_nf = 0;
       }
@@ -613,8 +620,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       PDZ_P(sp[4] += 1; sp[5] += clock64() - t_iss[dn & 3];)
       ++dn;
       progressed = true;
+      PDZ_P(lap(6);)
     }
-    PDZ_P(lap(0);)
     // 2. generate the schedule ahead (at most 3 blocks not yet done)
     bool wait_fin = false;
     while (!aborted && gen < dn + 3) {
@@ -624,8 +631,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         wait_fin = k == kIterWaitFin;
         // stop rule: the decisions of iteration n - 3 are needed; fin_probe
         // was loaded at the end of the previous round (its latency hidden)
-        if (wait_fin && fin_probe > fin_seen) {
-          fence_acq_rel_gpu();  // acquire: the stop records
+        if (wait_fin && fin_probe > fin_seen) {  // (loaded with acquire: the stop records)
           fin_seen = fin_probe;
           if (!anystop && a.st.running[0] < a.P) anystop = true;  // written before fin
           progressed = true;
@@ -678,7 +684,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     // stop rule: probe fin for the next round while the iterator waits for it
     // (in flight together with the scan loads)
     int fprobe = 0;
-    if (wait_fin && lane == 0) fprobe = ld_relaxed(a.fin);
+    if (wait_fin) fprobe = ld_acquire_gpu(a.fin);  // every lane: they all read the records
     PDZ_P(lap(2);)
     // 4. grant: every dependency met -> the TMA (before the publication, whose
     // release fence would otherwise delay it)
@@ -711,7 +717,10 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     // this warp, and the partials above)
     const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
     if (upto > published) {
+      PDZ_P(lap(5);)
       if (lane == 0) st_release(a.done + blockIdx.x, upto);
+      __syncwarp();
+      PDZ_P(lap(7);)
       PDZ_P(if (lane == 0) for (int kk = published + 1; kk <= upto; ++kk)
                 PDZ_TL(a, 0, blockIdx.x, kk);)
       PDZ_P(sp[2] += 1;)
@@ -730,16 +739,22 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       }
       PDZ_P(if (a.prof && lane == 0) {
         for (int i = 0; i < 8; ++i) a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + i] = sp[i];
-        for (int i = 0; i < 6; ++i) a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + 8 + i] = rp[i];
+        for (int i = 0; i < 8; ++i) a.prof[(2 * a.pt.G + 2 + blockIdx.x) * 16 + 8 + i] = rp[i];
       })
       return;
     }
     if (progressed) {
-      t0 = global_ns();
+      idle = 0;
       PDZ_P(lap(5);)
       continue;
     }
-    if (!aborted && (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs)) {
+    // nothing moved: the abort flag and the clock cost a global round trip
+    // each, so they are looked at every 64th idle round only
+    if ((++idle & 63) == 1) {
+      if (idle == 1) t0 = global_ns();
+    }
+    if (!aborted && (idle & 63) == 0 &&
+        (ld_relaxed(a.flags + 1) || global_ns() - t0 > kSpinTimeoutNs)) {
       // a dependency never arrived (or another CTA gave up): flag the abort,
       // stop generating, let the issued blocks drain and end the stream --
       // the launch completes, the host raises, the context stays usable
@@ -923,7 +938,7 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
     if (tid == kComputeThreads - 32) {
       // the C channels of an image share lambda: kept while the block covers
       // the same rows of the same image
-      const int img = cur.p / a.C;
+      const int img = cur.img;
       const bool lam = img != lam_img || cur.yb != lam_yb || cur.x0 != lam_x0;
       mbar_expect_tx(&bars[2], (lam ? 2u : 1u) * Gm::PL_FLOATS * 4u);
       tma_load_3d(sphi, &a.tm_phi, cur.x0, cur.yb, cur.p, &bars[2]);
@@ -1050,8 +1065,12 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int t = j - 2 * m;
+#ifdef PDZ_KO_COMPUTE  // timing-only build (profiles/r2_knockouts.txt): no arithmetic
+          if (t == R) o[m] = make_float2(v[OFF + j], v[OFF + j + 1]);
+#else
           if (t >= 0 && t <= 2 * R + 1)
             o[m] = ffma2(make_float2(v[OFF + j], v[OFF + j]), a.wp[t], o[m]);
+#endif
         }
       }
       float4* dst = reinterpret_cast<float4*>(h_cur + i * Gm::HP + 8 * g);
@@ -1082,7 +1101,11 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
 #pragma unroll
         for (int j = 0; j < kRPW; ++j) {
           const int t = k - j;
+#ifdef PDZ_KO_COMPUTE
+          if (t == R) G2[j] = hv;
+#else
           if (t >= 0 && t <= 2 * R) G2[j] = ffma2(a.w2[t], hv, G2[j]);
+#endif
         }
       }
 
@@ -1164,8 +1187,12 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
           // div0 = ((fm - fw) + s0) - n0, div1 = ((fe - fm) + s1) - n1, with
           // fe - fm = -(fm + (-fe)) exactly; the south and north fluxes
           // s = jd * rd, n = ju * ru enter as fused multiply-adds
+#ifdef PDZ_KO_COMPUTE
+          const float2 div = cC;
+#else
           const float2 we = make_float2(__fsub_rn(fm, fwe.x), -__fadd_rn(fm, fwe.y));
           const float2 div = ffma2(make_float2(-ju.x, -ju.y), ru, ffma2(jd, rd, we));
+#endif
           const float2 cB_old = cB;
           ju = jd;
           ru = rd;

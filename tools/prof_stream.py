@@ -73,5 +73,5 @@ n8, s9, n10, s11 = (w0[:, 8].sum(), w0[:, 9].sum(), w0[:, 10].sum(), w0[:, 11].s
 print(f"warp0 waits: {n8/G/iters:.2f}/sweep found the load unissued (avg issue {s9/max(n8,1):.0f} cyc after wait start); "
       f"{n10/G/iters:.2f}/sweep waited on an issued load (avg ready {s11/max(n10,1):.0f} cyc after issue)")
 
-rp = sv[:, 8:14].astype(float) / iters
-print("service round cycles per sweep: done %.0f  gen %.0f  scan %.0f  grant+tma %.0f  sleep %.0f  publish+rest %.0f" % tuple(rp.mean(axis=0)))
+rp = sv[:, 8:16].astype(float) / iters
+print("service round cycles per sweep: done-test %.0f  gen %.0f  scan %.0f  grant+tma %.0f  sleep %.0f  rest %.0f  reduce %.0f  release-store %.0f" % tuple(rp.mean(axis=0)))
