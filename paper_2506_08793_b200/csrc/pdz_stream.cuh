@@ -343,7 +343,8 @@ struct RangeIter {
   int L, L0, L1, b, s, y;
   int b0, s0, y0;
   bool check_stop;  // some plane has stopped: look up frozen planes (uniform per pass)
-  __device__ __forceinline__ void init(int l0, int l1, const StreamArgs& a) {
+  template <class A>
+  __device__ __forceinline__ void init(int l0, int l1, const A& a) {
     L = L0 = l0;
     L1 = l1;
     check_stop = false;
@@ -359,15 +360,16 @@ struct RangeIter {
     s = s0;
     y = y0;
   }
-  __device__ __forceinline__ void wrap(const StreamArgs& a) {
+  template <class A>
+  __device__ __forceinline__ void wrap(const A& a) {
     y = 0;
     if (++s == a.nstrips) {
       s = 0;
       ++b;
     }
   }
-  template <bool STOP>
-  __device__ __forceinline__ bool next(const StreamArgs& a, int iter, int c, SBlock& blk) {
+  template <bool STOP, class A>
+  __device__ __forceinline__ bool next(const A& a, int iter, int c, SBlock& blk) {
     while (L < L1) {
       const int seg_end = min(L1, L - y + a.H);
       const int p = b * a.C + c;
@@ -393,6 +395,36 @@ struct RangeIter {
   }
 };
 
+// The few kernel arguments the service warp's iterator reads on every block,
+// copied into registers once: read as kernel parameters they are constant-bank
+// loads, and the compute warps' tap streams keep evicting those lines, so a
+// handful of them per block cost the service warp ~1k cycles.
+__device__ __forceinline__ int reg_copy(int v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T* reg_copy(T* p) {
+  asm volatile("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
+struct SvcView {
+  int H, C, srb, nstrips, iter_last;
+  struct {
+    int32_t* stop_iter;
+  } st;
+  int32_t* flags;
+  __device__ __forceinline__ explicit SvcView(const StreamArgs& a) {
+    H = reg_copy(a.H);
+    C = reg_copy(a.C);
+    srb = reg_copy(a.srb);
+    nstrips = reg_copy(a.nstrips);
+    iter_last = reg_copy(a.iter_last);
+    st.stop_iter = reg_copy(a.st.stop_iter);
+    flags = reg_copy(a.flags);
+  }
+};
+
 // Progress counter value once pass (n, c) is complete.
 __device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter - 1) * C + c + 1; }
 
@@ -407,8 +439,8 @@ struct SvcIter {
   int iter, c;
   bool fresh;  // the next block starts a new pass
   bool ended;
-  template <bool STOP>
-  __device__ __forceinline__ int next(const StreamArgs& a, SBlock& blk, int fin_seen,
+  template <bool STOP, class A>
+  __device__ __forceinline__ int next(const A& a, SBlock& blk, int fin_seen,
                                       bool anystop) {
     while (!ended && iter <= a.iter_last) {
       if (STOP && fresh && a.st.stop_iter && iter > kNBuf) {
@@ -440,7 +472,8 @@ struct SvcIter {
     return kIterEnd;
   }
   // Progress index of the last pass before the iterator position.
-  __device__ __forceinline__ int completed(const StreamArgs& a) const {
+  template <class A>
+  __device__ __forceinline__ int completed(const A& a) const {
     return ended ? pass_index(a.iter_last, a.C - 1, a.C) : pass_index(iter, c, a.C) - 1;
   }
 };
@@ -546,10 +579,13 @@ template <int R, int V, bool STOP>
 __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float* in1,
                              uint64_t* bars, const DepSet& dep, int L0, int L1) {
   const int lane = threadIdx.x & 31;
-  const int C = a.C;
+  const int C = reg_copy(a.C);
   const bool fin_on = a.st.stop_iter != nullptr;
+  int32_t* const done_ctr = reg_copy(a.done);
+  int32_t* const fin_ctr = reg_copy(a.fin);
   SvcIter it;
-  it.r.init(L0, L1, a);
+  const SvcView sv(a);
+  it.r.init(L0, L1, sv);
   it.iter = 1;  // pass numbering (done[], grants) starts at sweep 1
   it.c = 0;
   it.fresh = true;
@@ -626,7 +662,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     bool wait_fin = false;
     while (!aborted && gen < dn + 3) {
       SBlock nb;
-      const int k = it.template next<STOP>(a, nb, fin_seen, anystop);
+      const int k = it.template next<STOP>(sv, nb, fin_seen, anystop);
       if (k != kIterBlock) {
         wait_fin = k == kIterWaitFin;
         // stop rule: the decisions of iteration n - 3 are needed; fin_probe
@@ -666,25 +702,25 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
         need = kpass - C;  // pass (n-1, c)
         if (b.iter >= 2) {
           if (ndep <= 64) {
-            if (dep0 >= 0) v0 = ld_acquire_gpu(a.done + dep0);
-            if (dep1 >= 0) v1 = ld_acquire_gpu(a.done + dep1);
+            if (dep0 >= 0) v0 = ld_acquire_gpu(done_ctr + dep0);
+            if (dep1 >= 0) v1 = ld_acquire_gpu(done_ctr + dep1);
           } else {
             bool ok = true;
 #pragma unroll
             for (int i = 0; i < 3; ++i)
               for (int j = dep.lo[i] + lane; j <= dep.hi[i]; j += 32)
-                ok &= ld_acquire_gpu(a.done + j) >= need;
+                ok &= ld_acquire_gpu(done_ctr + j) >= need;
             v0 = ok ? 0x7fffffff : -1;
           }
         }
         need_fin = b.iter - kRing;
-        if (fin_on && !STOP && need_fin > 0) vf = ld_acquire_gpu(a.fin);
+        if (fin_on && !STOP && need_fin > 0) vf = ld_acquire_gpu(fin_ctr);
       }
     }
     // stop rule: probe fin for the next round while the iterator waits for it
     // (in flight together with the scan loads)
     int fprobe = 0;
-    if (wait_fin) fprobe = ld_acquire_gpu(a.fin);  // every lane: they all read the records
+    if (wait_fin) fprobe = ld_acquire_gpu(fin_ctr);  // every lane: they all read the records
     PDZ_P(lap(2);)
     // 4. grant: every dependency met -> the TMA (before the publication, whose
     // release fence would otherwise delay it)
@@ -715,10 +751,10 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     // 5. progress: every pass before the oldest pending block is complete;
     // one release store (the block outputs the done barrier made visible to
     // this warp, and the partials above)
-    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(a);
+    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(sv);
     if (upto > published) {
       PDZ_P(lap(5);)
-      if (lane == 0) st_release(a.done + blockIdx.x, upto);
+      if (lane == 0) st_release(done_ctr + blockIdx.x, upto);
       __syncwarp();
       PDZ_P(lap(7);)
       PDZ_P(if (lane == 0) for (int kk = published + 1; kk <= upto; ++kk)
@@ -731,7 +767,7 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     PDZ_P(lap(5);)
     // 6. end of the stream: everything done and published (or, after an
     // abort, every issued block done: the compute warps then leave cleanly)
-    if ((it.ended && dn == gen && iss == gen && published >= it.completed(a)) ||
+    if ((it.ended && dn == gen && iss == gen && published >= it.completed(sv)) ||
         (aborted && dn == iss)) {
       if (lane == 0) {
         mb->desc[iss & 1].n = 0;
