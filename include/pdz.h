@@ -291,8 +291,10 @@ int32_t pdz_sweep_kernel_kind(const pdz_solve_params* params);
  * or tiles for the tiled kernel), CTAs per strip (kps; 0 = even split of
  * strip-rows, ranges may span strips and images), border bonus, block
  * geometry V, radius R, partial slots per plane, strips per image, output
- * rows per block, threads per CTA, stop rule armed}. */
-#define PDZ_PLAN_INFO_LEN 11
+ * rows per block, threads per CTA, stop rule armed, channel-inner block
+ * order (1: (iteration, block, channel), the channel blocks of a position
+ * share one lambda tile; 0: (iteration, channel, block))}. */
+#define PDZ_PLAN_INFO_LEN 12
 int32_t pdz_solve_plan_info(const pdz_solve_params* params, int32_t* info_host, int32_t n);
 /* Name of the sweep kernel template `params` launches (e.g.
  * "pdz::stream_kernel<9, 0, 1, 1>"), NUL-terminated into buf_host[n]. */

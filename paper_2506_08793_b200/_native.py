@@ -160,7 +160,8 @@ def check(rc: int) -> None:
 
 
 PLAN_FIELDS = ("kind", "ctas", "ctas_per_strip", "bonus", "geometry", "radius",
-               "partials_per_plane", "strips", "block_rows", "threads", "stop_rule")
+               "partials_per_plane", "strips", "block_rows", "threads", "stop_rule",
+               "channel_inner")
 
 
 def plan_info(params) -> dict:

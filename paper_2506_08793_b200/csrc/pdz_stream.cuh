@@ -133,6 +133,7 @@ struct StreamArgs {
   int32_t iter_last, max_iters;  // sweeps 1..iter_last
   int32_t srb;          // output rows per block (geo_srb(R, V))
   int32_t stop_rule;    // rel_tol active: pass (n, c) needs fin >= n - 2
+  int32_t chan_inner;   // block order (iteration, block, channel) instead of (iteration, channel, block)
   int32_t cnt_lo, cnt_hi;  // rows whose r^2 / non-finite flags are counted (0, H: all)
   float eps, tau;
   double rel_tol;
@@ -393,6 +394,37 @@ struct RangeIter {
     }
     return false;
   }
+  // Channel-inner order: the next block POSITION of the range and the mask of
+  // its image's channels still running (segments whose planes are all frozen
+  // are skipped).  blk.p = the image's first plane.
+  template <bool STOP, class A>
+  __device__ __forceinline__ bool next_pos(const A& a, int iter, SBlock& blk, int& mask) {
+    while (L < L1) {
+      const int seg_end = min(L1, L - y + a.H);
+      mask = (1 << a.C) - 1;
+      if (STOP && check_stop) {
+        for (int c = 0; c < a.C; ++c) {
+          const int st = a.st.stop_iter[b * a.C + c];
+          if (st != 0 && st <= iter - kNBuf) mask &= ~(1 << c);
+        }
+        if (mask == 0) {
+          L = seg_end;
+          wrap(a);
+          continue;
+        }
+      }
+      blk.p = b * a.C;
+      blk.img = b;
+      blk.x0 = s * kSTW;
+      blk.yb = y;
+      blk.n = min(a.srb, seg_end - L);
+      L += blk.n;
+      y += blk.n;
+      if (y == a.H) wrap(a);
+      return true;
+    }
+    return false;
+  }
 };
 
 // The few kernel arguments the service warp's iterator reads on every block,
@@ -409,12 +441,13 @@ __device__ __forceinline__ T* reg_copy(T* p) {
   return p;
 }
 struct SvcView {
-  int H, C, srb, nstrips, iter_last;
+  int H, C, srb, nstrips, iter_last, ci;
   struct {
     int32_t* stop_iter;
   } st;
   int32_t* flags;
   __device__ __forceinline__ explicit SvcView(const StreamArgs& a) {
+    ci = reg_copy(a.chan_inner);
     H = reg_copy(a.H);
     C = reg_copy(a.C);
     srb = reg_copy(a.srb);
@@ -428,17 +461,35 @@ struct SvcView {
 // Progress counter value once pass (n, c) is complete.
 __device__ __forceinline__ int pass_index(int iter, int c, int C) { return (iter - 1) * C + c + 1; }
 
+// Progress value that the CTAs a block reads from must have published, and
+// that is published once the block's own unit is complete.  Channel-outer
+// order: the unit is the pass (n, c) and it needs the neighbours' pass
+// (n-1, c).  Channel-inner order: the channels of a sweep complete together,
+// so the unit is the sweep: every block of sweep n carries (n-1) C + 1 and
+// needs (n-1) C, the neighbours' whole previous sweep.
+__device__ __forceinline__ int prog_index(int iter, int c, int C, int ci) {
+  return ci ? (iter - 1) * C + 1 : pass_index(iter, c, C);
+}
+__device__ __forceinline__ int prog_need(int kprog, int C, int ci) { return ci ? kprog - 1 : kprog - C; }
+
 // Flat stream of (iteration, channel, block) run by the service warp.
 // Passes with no blocks (every plane of the range frozen) are skipped.  With
 // the stop rule a pass of iteration n first needs the stop decisions of
 // n - 3 (fin >= n - 3: its answer buffer is then final); next() returns
 // kWaitFin until they are known.
 enum { kIterEnd = 0, kIterBlock = 1, kIterWaitFin = 2 };
+// Channel-inner order (a.ci; CTAs that walk several blocks per pass): the
+// stream is (iteration, block position, channel), so the three channel
+// blocks of a position run back to back and share one lambda tile (lambda is
+// a third of the Phi / lambda / u traffic of a block and was re-read for every
+// channel: measured DRAM traffic 1.4x algorithmic on configs 3 and 4).
 struct SvcIter {
   RangeIter r;
   int iter, c;
-  bool fresh;  // the next block starts a new pass
+  bool fresh;  // the next block starts a new pass (channel-inner: a new sweep)
   bool ended;
+  SBlock pos;  // channel-inner: the current block position
+  int mask;    // and its channels still to emit
   template <bool STOP, class A>
   __device__ __forceinline__ int next(const A& a, SBlock& blk, int fin_seen,
                                       bool anystop) {
@@ -454,6 +505,25 @@ struct SvcIter {
             break;
           }
         }
+      }
+      if (a.ci) {
+        if (mask == 0) {
+          if (!r.template next_pos<STOP>(a, iter, pos, mask)) {
+            ++iter;
+            r.reset();
+            fresh = true;
+            continue;
+          }
+          c = 0;
+        }
+        while (!(mask & (1 << c))) ++c;
+        mask &= ~(1 << c);
+        blk = pos;
+        blk.p = pos.p + c;
+        blk.iter = iter;
+        blk.c = c;
+        fresh = false;
+        return kIterBlock;
       }
       if (r.template next<STOP>(a, iter, c, blk)) {
         blk.iter = iter;
@@ -474,7 +544,8 @@ struct SvcIter {
   // Progress index of the last pass before the iterator position.
   template <class A>
   __device__ __forceinline__ int completed(const A& a) const {
-    return ended ? pass_index(a.iter_last, a.C - 1, a.C) : pass_index(iter, c, a.C) - 1;
+    if (ended) return pass_index(a.iter_last, a.C - 1, a.C);
+    return a.ci ? (iter - 1) * a.C : pass_index(iter, c, a.C) - 1;
   }
 };
 
@@ -590,6 +661,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
   it.c = 0;
   it.fresh = true;
   it.ended = false;
+  it.mask = 0;
+  const int ci = sv.ci;
   // flattened dependency list: lane l checks CTAs #l and #l + 32 of the
   // (disjoint) intervals; more than 64: the generic per-interval loop
   int ndep = 0, dep0 = -1, dep1 = -1;
@@ -621,6 +694,30 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     }
     acc_p = -1;
   };
+  // channel-inner order: the blocks of an image's channels alternate, so the
+  // open partials are per channel, keyed by (image, iteration)
+  double cacc0 = 0.0, cacc1 = 0.0, cacc2 = 0.0, cacc3 = 0.0;
+  int cmask = 0, cnf = 0, c_img = -1, c_it = 0;
+  auto flush_ci = [&]() {
+    if (cmask == 0) return;
+    if (lane == 0) {
+      if (c_img != slot_img) {
+        slot_img = c_img;
+        slot_k = int(blockIdx.x - part_cta_of(a.pt, int64_t(c_img) * a.pt.U));
+      }
+      const double v[4] = {cacc0, cacc1, cacc2, cacc3};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (cmask >> c & 1) {
+          const size_t slot =
+              (size_t(c_it & (kRing - 1)) * a.P + c_img * C + c) * a.pt.nbmax + slot_k;
+          a.pt.sum[slot] = v[c];
+          a.pt.flag[slot] = cnf >> c & 1;
+        }
+    }
+    cmask = 0;
+    cnf = 0;
+  };
   long long t0 = global_ns();
   int idle = 0;
   // [0] rounds [1] dependency-scan cycles [2] publications [3] sleeps
@@ -643,16 +740,29 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
       // result is the one stored: deterministic)
       const double s = warp_sum(lane < geo_scw(V) ? mb->red[dn & 1][lane] : 0.0);
       const int f = __any_sync(0xffffffffu, lane < geo_scw(V) && mb->nf[dn & 1][lane] != 0);
-      if (acc_p != b.p || acc_it != b.iter) {
-        flush();
-        acc_p = b.p;
-        acc_it = b.iter;
-        acc_img = b.img;
-        acc = 0.0;
-        acc_nf = 0;
+      if (ci) {
+        if (cmask != 0 && (c_img != b.img || c_it != b.iter)) flush_ci();
+        c_img = b.img;
+        c_it = b.iter;
+        const bool had = cmask >> b.c & 1;
+        if (b.c == 0) cacc0 = had ? cacc0 + s : s;
+        if (b.c == 1) cacc1 = had ? cacc1 + s : s;
+        if (b.c == 2) cacc2 = had ? cacc2 + s : s;
+        if (b.c == 3) cacc3 = had ? cacc3 + s : s;
+        cmask |= 1 << b.c;
+        cnf |= (f ? 1 : 0) << b.c;
+      } else {
+        if (acc_p != b.p || acc_it != b.iter) {
+          flush();
+          acc_p = b.p;
+          acc_it = b.iter;
+          acc_img = b.img;
+          acc = 0.0;
+          acc_nf = 0;
+        }
+        acc += s;
+        acc_nf |= f;
       }
-      acc += s;
-      acc_nf |= f;
       PDZ_P(sp[4] += 1; sp[5] += clock64() - t_iss[dn & 3];)
       ++dn;
       progressed = true;
@@ -685,6 +795,9 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     if (acc_p >= 0 && (dn < gen ? (q[dn & 3].p != acc_p || q[dn & 3].iter != acc_it)
                                 : (it.fresh || it.ended)))
       flush();
+    if (cmask != 0 && (dn < gen ? (q[dn & 3].img != c_img || q[dn & 3].iter != c_it)
+                                : (it.fresh || it.ended)))
+      flush_ci();
     PDZ_P(lap(1);)
     // 3. scan for the next TMA load (block iss): acquire loads of the
     // neighbours' progress, one per lane (the flattened dependency list; an
@@ -695,11 +808,11 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     bool scan = false;
     if (want) {
       const SBlock& b = q[iss & 3];
-      kpass = pass_index(b.iter, b.c, C);
+      kpass = prog_index(b.iter, b.c, C, ci);
       PDZ_P(if (lane == 0 && want_k != kpass) { want_k = kpass; PDZ_TL(a, 2, blockIdx.x, kpass); })
       if (kpass > granted_k) {
         scan = true;
-        need = kpass - C;  // pass (n-1, c)
+        need = prog_need(kpass, C, ci);  // pass (n-1, c) / the whole sweep n-1
         if (b.iter >= 2) {
           if (ndep <= 64) {
             if (dep0 >= 0) v0 = ld_acquire_gpu(done_ctr + dep0);
@@ -751,7 +864,8 @@ __device__ void service_loop(const StreamArgs& a, Mailbox* mb, float* in0, float
     // 5. progress: every pass before the oldest pending block is complete;
     // one release store (the block outputs the done barrier made visible to
     // this warp, and the partials above)
-    const int upto = dn < gen ? pass_index(q[dn & 3].iter, q[dn & 3].c, C) - 1 : it.completed(sv);
+    const int upto =
+        dn < gen ? prog_index(q[dn & 3].iter, q[dn & 3].c, C, ci) - 1 : it.completed(sv);
     if (upto > published) {
       PDZ_P(lap(5);)
       if (lane == 0) st_release(done_ctr + blockIdx.x, upto);
@@ -1307,7 +1421,9 @@ template <int V, bool EDGE, bool STOP>
 static StreamFn stream_pick_radius(int R, size_t* smem) {
   switch (R) {  // radii whose staging fits in shared memory (SGeo<R, V>::FITS)
 #ifdef PDZ_ONLY_R  // experiment builds (tools/): one radius, a minute to compile
-    case PDZ_ONLY_R: return stream_prepared<PDZ_ONLY_R, PDZ_ONLY_R == 24 ? 0 : V, EDGE, STOP>(smem);
+    case PDZ_ONLY_R:
+      if (PDZ_ONLY_R > 12 && V != 0) return nullptr;  // like the full table: V = 1 up to R = 12
+      return stream_prepared<PDZ_ONLY_R, (PDZ_ONLY_R > 12) ? 0 : V, EDGE, STOP>(smem);
 #else
     case 1: return stream_prepared<1, V, EDGE, STOP>(smem);
     case 2: return stream_prepared<2, V, EDGE, STOP>(smem);

@@ -352,6 +352,7 @@ struct Plan {
   int pad_r = 0, pad_c = 0;                 // iterate buffer pads (rows, columns)
   int ring = 2;                             // iteration slots of the partials
   int geo = 0;                              // block geometry V (pdz_stream.cuh)
+  int ci = 0;                               // channel-inner block order (pdz_stream.cuh)
   size_t smem = 0;
   void* fn = nullptr;
 };
@@ -536,9 +537,23 @@ static int32_t check_params(const pdz_solve_params* p, Plan* pl, bool allow_stre
       }
       cudaGetLastError();
     }
+    // Block order: CTAs that walk many blocks per pass run the channels of a
+    // block position back to back (one lambda tile for the C channel blocks:
+    // 14 % less DRAM traffic).  The neighbour dependency is then per sweep,
+    // which costs one pipeline refill per sweep: measured +3.2 % on config 3
+    // (70 blocks per pass and CTA) but -3 % on config 4 (7 blocks), so the
+    // order is used from 24 blocks per pass on, and not for the FP32-bound
+    // large radii (config 5, K = 49: 773 vs 771 us).  Everything else keeps
+    // the channel-outer order, whose dependencies are C - 1 passes old.
+    P.ci = (p->channels >= 2 && p->channels <= 4 && P.R <= 12 &&
+            P.S / std::max(1, P.G) >= 24 * int64_t(geo_srb(P.R, P.geo))) ? 1 : 0;
+    if (const char* e = getenv("PDZ_STREAM_CI")) P.ci = (atoi(e) != 0 && p->channels >= 2 &&
+                                                         p->channels <= 4) ? 1 : 0;
     if (getenv("PDZ_VERBOSE"))
-      fprintf(stderr, "pdz: plan G=%d kps=%d bonus=%d geometry=%d cost=%lld max_segment=%lld\n",
-              P.G, P.kps, P.bonus, P.geo, (long long)cost, (long long)max_seg);
+      fprintf(stderr,
+              "pdz: plan G=%d kps=%d bonus=%d geometry=%d channel_inner=%d cost=%lld "
+              "max_segment=%lld\n",
+              P.G, P.kps, P.bonus, P.geo, P.ci, (long long)cost, (long long)max_seg);
   } else {
     cudaGetLastError();  // clear a failed occupancy query
     P.stream = false;
@@ -701,6 +716,7 @@ static int32_t fill_args(const pdz_solve_params* p, const Plan& pl, float* buf0,
   b.iter_last = p->max_iters;
   b.max_iters = p->max_iters;
   b.stop_rule = (p->rel_tol >= 0.0) ? 1 : 0;
+  b.chan_inner = pl.ci;
   b.cnt_lo = 0;
   b.cnt_hi = p->height;
 #ifdef PDZ_PROFILE
@@ -1438,6 +1454,7 @@ int32_t pdz_solve_plan_info(const pdz_solve_params* params, int32_t* info_host, 
       pl.stream ? geo_srb(pl.R, pl.geo) : kTH,
       pl.stream ? geo_threads(pl.geo) : kThreads,
       rel ? 1 : 0,
+      pl.ci,
   };
   for (int i = 0; i < n && i < PDZ_PLAN_INFO_LEN; ++i) info_host[i] = v[i];
   return PDZ_OK;

@@ -244,3 +244,32 @@ def test_dehaze_slabs_single_rank(pdz):
             assert x.residual_norms == y.residual_norms
             assert x.iterations_run == y.iterations_run
         _check_against_oracle(out, info, img, cfg)
+
+
+@pytest.mark.parametrize("rel_tol", [1e-300, 3e-3])
+def test_channel_inner_block_order(pdz, monkeypatch, rel_tol):
+    """Config 3 runs its blocks in (iteration, block, channel) order (one
+    lambda tile for the three channel blocks of a position; the neighbour
+    dependency is per sweep).  Forced on and off for the same batch: the
+    restored images are bitwise equal (the order changes no arithmetic), the
+    norms agree to 1e-8, iterations_run are equal; and the real 256-image
+    plan has the order switched on."""
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import _params
+
+    cfg = _cfg(pdz, 3, rel_tol=rel_tol, max_iters=60)
+    assert nat.plan_info(_params(480, 640, 3 * 256, 3, _cfg(pdz, 3)))["channel_inner"] == 1
+    assert nat.plan_info(_params(1024, 1024, 3, 3, _cfg(pdz, 2)))["channel_inner"] == 0
+    imgs = _c3_batch(pdz, 12)
+    runs = {}
+    for ci in ("0", "1"):
+        monkeypatch.setenv("PDZ_STREAM_CI", ci)
+        assert _c3_plan(pdz, 12, cfg)["channel_inner"] == int(ci)
+        runs[ci] = pdz.dehaze_batch(imgs, cfg, ablation=FLAGS)
+    np.testing.assert_array_equal(runs["0"][0], runs["1"][0])
+    for a, b in zip(runs["0"][1], runs["1"][1]):
+        for x, y in zip(a.traces, b.traces):
+            assert x.iterations_run == y.iterations_run and x.converged == y.converged
+            np.testing.assert_allclose(x.residual_norms, y.residual_norms, rtol=1e-8)
+    monkeypatch.setenv("PDZ_STREAM_CI", "1")
+    _check_against_oracle(runs["1"][0][3], runs["1"][1][3], imgs[3], cfg)
