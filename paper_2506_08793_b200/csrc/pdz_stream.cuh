@@ -1049,6 +1049,16 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
   uint32_t ph_in = 0, ph_pl = 0;  // bit ib: phase of IN(ib)
   int ib = 0;
   int lam_img = -1, lam_yb = -1, lam_x0 = -1;  // rows of the lambda tile held
+  // H rows carried from block to block down a strip (large radii only): the H
+  // buffer is a ring of ROWS rows, local row i of the block lives in physical
+  // row (i + hbase) % ROWS.  A block that continues the previous one (same
+  // plane and strip, yb = the previous yb + n) finds its first 2R rows there
+  // already -- they are the previous block's rows [n, n + 2R) -- and blurs
+  // only its n new rows: (n + 2R) / n = 1.5x less horizontal-pass work at
+  // K = 49.  (At R <= 12 the ring's address arithmetic costs more than the
+  // saved rows: measured slower on configs 3 and 4.)
+  constexpr bool kCarry = R > 12;
+  int hbase = 0, prev_p = -1, prev_x0 = 0, prev_end = 0, prev_yb = 0;
   // profile rows (PDZ_PROFILE builds): lane 0 of warps 0 and kSCW-1, clock64
   // [0] total [1] IN wait [2] H pass [3] H barrier [4] Phi/lambda wait
   // [5] V pass [6] report + end barrier [7] blocks
@@ -1108,6 +1118,20 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
     float acc_nf = 0.0f;
 
     const int hn = cur.n + 2 * R;
+    int hfirst = 0;  // first H row to blur
+    if (kCarry) {
+      if (cur.p == prev_p && cur.x0 == prev_x0 && cur.yb == prev_end) {
+        hbase += cur.yb - prev_yb;
+        if (hbase >= Gm::ROWS) hbase -= Gm::ROWS;
+        hfirst = 2 * R;
+      } else {
+        hbase = 0;
+      }
+      prev_p = cur.p;
+      prev_x0 = cur.x0;
+      prev_yb = cur.yb;
+      prev_end = cur.yb + cur.n;
+    }
     // ---- image borders (np.pad "symmetric", solver.py:235: -1-i <- i,
     // H+i <- H-1-i): nothing mirrored is stored globally and the pads of the
     // global iterates never carry data.  The horizontal pass reads a pad
@@ -1138,13 +1162,13 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
     // staged values per 8 outputs.
     // Item -> (row i, column group g): 8 consecutive items = 8 consecutive rows
     // of one group (a conflict-free quarter-warp, see SGeo).
-    const int hitems = ((hn + 7) & ~7) * (kSTW / 8);
+    const int hitems = ((hn - hfirst + 7) & ~7) * (kSTW / 8);
     constexpr int OFF = Gm::RP - R;
     constexpr int NQ = (OFF + 2 * R + 8 + 3) / 4;
     // staged values of one item -> registers (false: no such item)
     auto hfetch = [&](int item, float (&v)[4 * NQ], int& i, int& g) -> bool {
       if (item >= hitems) return false;
-      i = (item >> 6) * 8 + (item & 7);
+      i = hfirst + (item >> 6) * 8 + (item & 7);
       g = (item >> 3) & 7;
       if (i >= hn) return false;
       const int y = ylo + i;  // a pad row reads its mirror source row
@@ -1223,7 +1247,12 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
 #endif
         }
       }
-      float4* dst = reinterpret_cast<float4*>(h_cur + i * Gm::HP + 8 * g);
+      int hr = i;  // physical H row
+      if (kCarry) {
+        hr += hbase;
+        if (hr >= Gm::ROWS) hr -= Gm::ROWS;
+      }
+      float4* dst = reinterpret_cast<float4*>(h_cur + hr * Gm::HP + 8 * g);
       dst[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
       dst[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
     };
@@ -1245,9 +1274,23 @@ __global__ void __maxnreg__(geo_nreg(V))  // the whole register file: one CTA pe
       float2 G2[kRPW];
 #pragma unroll
       for (int j = 0; j < kRPW; ++j) G2[j] = make_float2(0.f, 0.f);
+      const float* hrow = h_cur + c;  // kCarry: walks the ring
+      if (kCarry) {
+        int hr = j0 + hbase;
+        if (hr >= Gm::ROWS) hr -= Gm::ROWS;
+        hrow += hr * Gm::HP;
+      }
+      const float* const hend = h_cur + Gm::ROWS * Gm::HP;
 #pragma unroll
       for (int k = 0; k < kRPW + 2 * R; ++k) {
-        const float2 hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * Gm::HP + c);
+        float2 hv;
+        if (kCarry) {
+          hv = *reinterpret_cast<const float2*>(hrow);
+          hrow += Gm::HP;
+          if (hrow >= hend) hrow -= Gm::ROWS * Gm::HP;
+        } else {
+          hv = *reinterpret_cast<const float2*>(h_cur + (j0 + k) * Gm::HP + c);
+        }
 #pragma unroll
         for (int j = 0; j < kRPW; ++j) {
           const int t = k - j;
