@@ -88,3 +88,30 @@ def test_oracle_not_imported_by_product():
                 text = open(os.path.join(root, f)).read()
                 for needle in ("import oracle", "from oracle", "pdz_oracle"):
                     assert needle not in text, (f, needle)
+
+
+def test_bench_workloads_and_shards():
+    """bench.py host logic: the `config` object is the same in both arms, the
+    image shards of config 3 cover the batch exactly once for every world
+    size, and the CPU arm's bounded sample is a crop of the config."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for n in (1, 2, 3, 4, 5):
+        w = bench._workload(n)
+        assert w == bench._workload(n) and w["config_number"] == n
+        assert set(w) >= {"workload", "height", "width", "kernel_size", "iterations", "l2"}
+        rows, cols = bench.cpu_sample_shape(n)
+        assert 1 <= rows <= w["height"] and 1 <= cols <= w["width"]
+        assert rows * cols * w["kernel_size"] ** 2 <= 2.1 * 1024 * 1024 * 19 * 19
+    assert bench._workload(5)["rel_tol"] == 1e-5 and bench._workload(2)["rel_tol"] is None
+    for world in (1, 2, 3, 4, 8):
+        seen = [i for r in range(world) for i in bench.shard(256, world, r)]
+        assert seen == list(range(256))
+        assert max(len(bench.shard(256, world, r)) for r in range(world)) == -(-256 // world)
+    assert bench._mode(3, 8)[1] == "strong" and bench._mode(2, 8)[1] == "weak"
+    assert "row slabs" in bench._mode(4, 4)[0] and "replicas" in bench._mode(4, 1)[0]
