@@ -112,6 +112,29 @@ int32_t pdz_atmospheric_light(const void* image, int32_t image_is_f64, int32_t h
 int32_t pdz_transmission(const double* dark, int32_t height, int32_t width, double omega,
                          double* transmission, void* stream);
 
+/* The whole front end of dehaze (solver.py:393-419 without the guided
+ * refinement) for a BATCH of equal-shaped images stored back to back
+ * ([batch][H][W][C]), every stage ONE launch sequence for the batch (the
+ * kernels take the image from the grid): (multiscale) dark channel at A = 1,
+ * the airlight selection, the dark channel normalised by each image's A, the
+ * transmission, and -- when the outputs are non-NULL -- Phi (planar float32
+ * [batch * C][H][W]), lambda (float32 [batch][H][W]) and the float64 Phi
+ * ([batch][H][W][C]).  radii / weights: the n_radii scales of
+ * multiscale_dark_channel (host arrays; one radius with weight 1 = the plain
+ * dark channel).  airlight: device float64 [batch][C]; transmission: device
+ * float64 [batch][H][W].  Each image's results are bitwise those of the
+ * single-image entry points.  Replaces the per-image loop of a caller that
+ * maps dehaze over a batch (BASELINE config 3). */
+size_t pdz_front_end_batch_workspace_bytes(int32_t batch, int32_t height, int32_t width,
+                                           int32_t n_radii, double fraction);
+int32_t pdz_front_end_batch(const void* images, int32_t image_is_f64, int32_t batch,
+                            int32_t height, int32_t width, int32_t channels,
+                            const int32_t* radii_host, const double* weights_host,
+                            int32_t n_radii, double fraction, double omega, double t_floor,
+                            int32_t lambda_mode, double lambda0, double beta, double* airlight,
+                            double* transmission, float* phi, float* lambda_map, double* phi64,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* Solver inputs for one image: Phi_c = (I_c - A_c (1 - t)) / max(t, t0)
  * (solver.py:324, scattering.py:138-139) as planar float32 [C][H][W], and
  * lambda(t) (solver.py:244-263 or the ablation overrides :414-417) as float32

@@ -93,6 +93,10 @@ _SIGNATURES = {
     "pdz_fixed_point_solve_async": (_i32, [_pp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_fixed_point_sweeps_from": (
         _i32, [_pp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "pdz_front_end_batch_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _f64]),
+    "pdz_front_end_batch": (
+        _i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _f64, _f64, _f64, _i32, _f64,
+               _f64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "pdz_slab_layout": (_i32, [_pp, _vp, _i32]),
     "pdz_fixed_point_sweeps_resident": (
         _i32, [_pp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),

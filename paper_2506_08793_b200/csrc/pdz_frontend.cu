@@ -27,14 +27,22 @@ __device__ __forceinline__ double load_f64(const void* p, size_t i) {
 }
 
 // ---------------------------------------------------------------- dark ---
+// Batched kernels: blockIdx.y (blockIdx.z for the transpose) is the image of a
+// batch of equal-shaped images stored back to back; the single-image entry
+// points launch them with one image.
 template <typename T>
 __global__ void chanmin_kernel(const void* __restrict__ img, int64_t n, int C,
-                               const double* __restrict__ airlight, double* __restrict__ out) {
+                               const double* __restrict__ airlight, int a_stride,
+                               double* __restrict__ out) {
+  const size_t z = blockIdx.y;
+  const double* a = airlight + z * a_stride;  // a_stride = 0: one vector for every image
+  const size_t ibase = z * size_t(n) * C;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    double m = __ddiv_rn(load_f64<T>(img, size_t(i) * C), airlight[0]);
-    for (int c = 1; c < C; ++c) m = fmin(m, __ddiv_rn(load_f64<T>(img, size_t(i) * C + c), airlight[c]));
-    out[i] = m;
+    double m = __ddiv_rn(load_f64<T>(img, ibase + size_t(i) * C), a[0]);
+    for (int c = 1; c < C; ++c)
+      m = fmin(m, __ddiv_rn(load_f64<T>(img, ibase + size_t(i) * C + c), a[c]));
+    out[z * size_t(n) + i] = m;
   }
 }
 
@@ -48,7 +56,8 @@ __global__ void chanmin_kernel(const void* __restrict__ img, int64_t n, int C,
 __global__ void rowmin_vhgw_kernel(const double* __restrict__ in, double* __restrict__ out,
                                    int H, int W, int r, int span) {
   extern __shared__ double sm[];
-  const int y = blockIdx.y;
+  const int y = blockIdx.y + blockIdx.z * gridDim.y;  // (a batch has more rows than grid.y holds)
+  if (y >= H) return;
   const int x0 = blockIdx.x * span;
   const int L = span + 2 * r;  // staged length
   double* g = sm;
@@ -79,8 +88,8 @@ __global__ void rowmin_vhgw_kernel(const double* __restrict__ in, double* __rest
 __global__ void rowmin_direct_kernel(const double* __restrict__ in, double* __restrict__ out,
                                      int H, int W, int r) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  if (x >= W) return;
+  const int y = blockIdx.y + blockIdx.z * gridDim.y;
+  if (x >= W || y >= H) return;
   const double* row = in + size_t(y) * W;
   double m = row[x];
   const int lo = max(0, x - r), hi = min(W - 1, x + r);
@@ -93,6 +102,8 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
                                  int W, int cap_at_one) {
   __shared__ double t[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  in += size_t(blockIdx.z) * H * W;
+  out += size_t(blockIdx.z) * H * W;
   for (int j = threadIdx.y; j < 32; j += blockDim.y) {
     const int y = by + j, x = bx + threadIdx.x;
     if (y < H && x < W) t[j][threadIdx.x] = in[size_t(y) * W + x];
@@ -108,13 +119,16 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
   }
 }
 
+constexpr int kRowGridY = 32768;  // rows per grid.y slab (grid.y <= 65535)
+
 static int32_t rowmin(const double* in, double* out, int H, int W, int r, cudaStream_t s) {
   if (r == 0) {
     PDZ_CUDA(cudaMemcpyAsync(out, in, size_t(H) * W * 8, cudaMemcpyDeviceToDevice, s), "copy");
     return PDZ_OK;
   }
   if (r > 2048) {
-    rowmin_direct_kernel<<<dim3((W + 255) / 256, H), 256, 0, s>>>(in, out, H, W, r);
+    rowmin_direct_kernel<<<dim3((W + 255) / 256, std::min(H, kRowGridY), (H + kRowGridY - 1) / kRowGridY),
+                           256, 0, s>>>(in, out, H, W, r);
     PDZ_CHECK_LAUNCH("rowmin direct");
     return PDZ_OK;
   }
@@ -124,14 +138,17 @@ static int32_t rowmin(const double* in, double* out, int H, int W, int r, cudaSt
   if (first_use_on_device(&raised))
     cudaFuncSetAttribute(rowmin_vhgw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          2 * (2048 + 2 * 2048) * 8);
-  rowmin_vhgw_kernel<<<dim3((W + span - 1) / span, H), 256, smem, s>>>(in, out, H, W, r, span);
+  rowmin_vhgw_kernel<<<dim3((W + span - 1) / span, std::min(H, kRowGridY),
+                            (H + kRowGridY - 1) / kRowGridY),
+                       256, smem, s>>>(in, out, H, W, r, span);
   PDZ_CHECK_LAUNCH("rowmin");
   return PDZ_OK;
 }
 
-static int32_t transpose(const double* in, double* out, int H, int W, bool cap, cudaStream_t s) {
-  transpose_kernel<<<dim3((W + 31) / 32, (H + 31) / 32), dim3(32, 8), 0, s>>>(in, out, H, W,
-                                                                              cap ? 1 : 0);
+static int32_t transpose(const double* in, double* out, int H, int W, bool cap, cudaStream_t s,
+                         int batch = 1) {
+  transpose_kernel<<<dim3((W + 31) / 32, (H + 31) / 32, batch), dim3(32, 8), 0, s>>>(
+      in, out, H, W, cap ? 1 : 0);
   PDZ_CHECK_LAUNCH("transpose");
   return PDZ_OK;
 }
@@ -144,21 +161,28 @@ static size_t dark_ws(int H, int W) {
   return Carver::round(c.off);
 }
 
+// `batch` images back to back (tmp_a / tmp_b / dark hold batch * H * W doubles);
+// airlight: [batch][C] with a_stride = C, or one [C] vector with a_stride = 0.
+// The row pass runs over the batch * H rows of the stacked images, the column
+// pass over the batch * W rows of the per-image transposes.
 static int32_t dark_channel_impl(const void* img, int is_f64, int H, int W, int C,
                                  const double* airlight, int r, double* dark, double* tmp_a,
-                                 double* tmp_b, cudaStream_t s) {
+                                 double* tmp_b, cudaStream_t s, int batch = 1,
+                                 int a_stride = 0) {
   const int64_t n = int64_t(H) * W;
-  const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+  const int gx = int(std::max<int64_t>(
+      1, std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8 / std::min(batch, 8))));
+  const dim3 grid(gx, batch);
   if (is_f64)
-    chanmin_kernel<double><<<grid, 256, 0, s>>>(img, n, C, airlight, tmp_a);
+    chanmin_kernel<double><<<grid, 256, 0, s>>>(img, n, C, airlight, a_stride, tmp_a);
   else
-    chanmin_kernel<float><<<grid, 256, 0, s>>>(img, n, C, airlight, tmp_a);
+    chanmin_kernel<float><<<grid, 256, 0, s>>>(img, n, C, airlight, a_stride, tmp_a);
   PDZ_CHECK_LAUNCH("chanmin");
   int32_t rc;
-  if ((rc = rowmin(tmp_a, tmp_b, H, W, r, s)) != PDZ_OK) return rc;
-  if ((rc = transpose(tmp_b, tmp_a, H, W, false, s)) != PDZ_OK) return rc;  // [W][H]
-  if ((rc = rowmin(tmp_a, tmp_b, W, H, r, s)) != PDZ_OK) return rc;
-  return transpose(tmp_b, dark, W, H, true, s);
+  if ((rc = rowmin(tmp_a, tmp_b, batch * H, W, r, s)) != PDZ_OK) return rc;
+  if ((rc = transpose(tmp_b, tmp_a, H, W, false, s, batch)) != PDZ_OK) return rc;  // [W][H]
+  if ((rc = rowmin(tmp_a, tmp_b, batch * W, H, r, s)) != PDZ_OK) return rc;
+  return transpose(tmp_b, dark, W, H, true, s, batch);
 }
 
 // combined = w0*d0 (first) or combined + w*d, float64 without contraction.
@@ -184,6 +208,7 @@ struct SelectState {
 };
 
 __global__ void select_init_kernel(SelectState* st, unsigned long long count) {
+  st += blockIdx.x;  // one state per image of a batch
   const int t = threadIdx.x;
   if (t == 0) {
     st->prefix = 0;
@@ -197,6 +222,8 @@ __global__ void select_hist_kernel(const double* __restrict__ dark, int64_t n, S
                                    int shift) {
   __shared__ unsigned int sh[256];
   sh[threadIdx.x] = 0;
+  dark += size_t(blockIdx.y) * n;
+  st += blockIdx.y;
   __syncthreads();
   const unsigned long long prefix = st->prefix, mask = st->mask;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -212,6 +239,7 @@ __global__ void select_hist_kernel(const double* __restrict__ dark, int64_t n, S
 __global__ void select_digit_kernel(SelectState* st, int shift) {
   __shared__ unsigned long long cnt[256];
   const int t = threadIdx.x;
+  st += blockIdx.x;
   cnt[t] = st->hist[255 - t];  // descending digit order
   __syncthreads();
   if (t == 0) {
@@ -234,6 +262,10 @@ __global__ void select_digit_kernel(SelectState* st, int shift) {
 __global__ void select_count_kernel(const double* __restrict__ dark, int64_t n,
                                     const SelectState* st, unsigned int* gt_cnt,
                                     unsigned int* eq_cnt) {
+  dark += size_t(blockIdx.y) * n;
+  st += blockIdx.y;
+  gt_cnt += size_t(blockIdx.y) * gridDim.x;
+  eq_cnt += size_t(blockIdx.y) * gridDim.x;
   const unsigned long long T = st->prefix;
   unsigned int gt = 0, eq = 0;
   const int64_t base = int64_t(blockIdx.x) * kSelBlock + int64_t(threadIdx.x) * kSelItems;
@@ -272,6 +304,8 @@ __global__ void select_count_kernel(const double* __restrict__ dark, int64_t n,
 // block (integer sums: any order is exact).
 __global__ void select_scan_kernel(unsigned int* gt_cnt, unsigned int* eq_cnt, int nblocks) {
   __shared__ unsigned int sg[1024], se[1024];
+  gt_cnt += size_t(blockIdx.x) * nblocks;
+  eq_cnt += size_t(blockIdx.x) * nblocks;
   const int t = threadIdx.x, nt = blockDim.x;
   const int per = (nblocks + nt - 1) / nt;
   const int lo = min(nblocks, t * per), hi = min(nblocks, lo + per);
@@ -307,6 +341,12 @@ __global__ void select_compact_kernel(const double* __restrict__ dark, int64_t n
                                       const SelectState* st, const unsigned int* gt_off,
                                       const unsigned int* eq_off, unsigned long long count,
                                       unsigned long long* cand_key, int64_t* cand_idx) {
+  dark += size_t(blockIdx.y) * n;
+  st += blockIdx.y;
+  gt_off += size_t(blockIdx.y) * gridDim.x;
+  eq_off += size_t(blockIdx.y) * gridDim.x;
+  cand_key += size_t(blockIdx.y) * count;
+  cand_idx += size_t(blockIdx.y) * count;
   const unsigned long long T = st->prefix;
   const unsigned long long need_eq = st->k;
   const unsigned long long n_gt = count - need_eq;
@@ -370,6 +410,9 @@ __global__ void select_rank_kernel(const unsigned long long* __restrict__ cand_k
                                    int64_t* __restrict__ sorted_idx) {
   __shared__ unsigned long long sk[256];
   __shared__ int64_t si[256];
+  cand_key += size_t(blockIdx.y) * m;
+  cand_idx += size_t(blockIdx.y) * m;
+  sorted_idx += size_t(blockIdx.y) * m;
   const int q = threadIdx.x & 3;
   const int64_t i = int64_t(blockIdx.x) * 64 + (threadIdx.x >> 2);
   const unsigned long long ki = i < m ? cand_key[i] : 0ull;
@@ -400,10 +443,13 @@ __global__ void select_rank_kernel(const unsigned long long* __restrict__ cand_k
 template <typename T>
 __global__ void airlight_gather_kernel(const void* __restrict__ img, int C,
                                        const int64_t* __restrict__ sorted_idx, int64_t m,
-                                       double* __restrict__ vals) {
+                                       double* __restrict__ vals, int64_t n) {
+  sorted_idx += size_t(blockIdx.y) * m;
+  vals += size_t(blockIdx.y) * 32 * m;
+  const size_t ibase = size_t(blockIdx.y) * n * C;
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += int64_t(gridDim.x) * blockDim.x) {
-    const size_t base = size_t(sorted_idx[j]) * C;
+    const size_t base = ibase + size_t(sorted_idx[j]) * C;
     for (int c = 0; c < C; ++c) vals[size_t(c) * m + j] = load_f64<T>(img, base + c);
   }
 }
@@ -439,6 +485,8 @@ __global__ void airlight_mean_kernel(const double* __restrict__ vals, int C, int
   constexpr int kChunk = 2048;
   __shared__ double sv[kChunk];
   const int c = blockIdx.x;
+  vals += size_t(blockIdx.y) * 32 * m;
+  airlight += size_t(blockIdx.y) * C;
   const double* v = vals + size_t(c) * m;
   double s = 0.0;
   if (C == 1) {
@@ -474,19 +522,21 @@ struct SelectLayout {
   size_t bytes;
 };
 
-static SelectLayout carve_select(int H, int W, double fraction, void* ws, size_t cap) {
+static SelectLayout carve_select(int H, int W, double fraction, void* ws, size_t cap,
+                                 int batch = 1) {
   Carver c(ws, cap);
   SelectLayout L;
   const int64_t n = int64_t(H) * W;
   const int64_t m = std::max<int64_t>(1, airlight_count(H, W, fraction));
   const int64_t nb = (n + kSelBlock - 1) / kSelBlock;
-  L.st = c.take<SelectState>(1);
-  L.gt = c.take<unsigned int>(nb);
-  L.eq = c.take<unsigned int>(nb);
-  L.ckey = c.take<unsigned long long>(m);
-  L.cidx = c.take<int64_t>(m);
-  L.sorted = c.take<int64_t>(m);
-  L.vals = c.take<double>(size_t(m) * 32);
+  const size_t B = size_t(batch);
+  L.st = c.take<SelectState>(B);
+  L.gt = c.take<unsigned int>(B * nb);
+  L.eq = c.take<unsigned int>(B * nb);
+  L.ckey = c.take<unsigned long long>(B * m);
+  L.cidx = c.take<int64_t>(B * m);
+  L.sorted = c.take<int64_t>(B * m);
+  L.vals = c.take<double>(B * size_t(m) * 32);
   L.bytes = c.off;
   return L;
 }
@@ -505,13 +555,20 @@ __global__ void fields_kernel(const void* __restrict__ img, int64_t n, int C,
                               double t_floor, int mode, double lambda0, double beta,
                               float* __restrict__ phi, float* __restrict__ lam,
                               double* __restrict__ phi64) {
+  const size_t z = blockIdx.y;  // image of a batch
+  const size_t ibase = z * size_t(n) * C;
+  t += z * size_t(n);
+  airlight += z * C;
+  if (phi) phi += z * size_t(n) * C;
+  if (lam) lam += z * size_t(n);
+  if (phi64) phi64 += z * size_t(n) * C;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const double ti = t[i];
     const double one_minus_t = __dsub_rn(1.0, ti);
     const double denom = fmax(ti, t_floor);
     for (int c = 0; c < C; ++c) {
-      const double v = __ddiv_rn(__dsub_rn(load_f64<T>(img, size_t(i) * C + c),
+      const double v = __ddiv_rn(__dsub_rn(load_f64<T>(img, ibase + size_t(i) * C + c),
                                            __dmul_rn(airlight[c], one_minus_t)),
                                  denom);
       if (phi) phi[size_t(c) * n + i] = float(v);
@@ -632,6 +689,36 @@ size_t pdz_airlight_workspace_bytes(int32_t height, int32_t width, double fracti
   return Carver::round(carve_select(height, width, fraction, nullptr, 0).bytes);
 }
 
+// A of `batch` images (dark: [batch][H][W], airlight out: [batch][C]).
+static int32_t airlight_impl(const void* image, int is_f64, int H, int W, int C,
+                             const double* dark, double fraction, double* airlight,
+                             const SelectLayout& L, cudaStream_t s, int batch) {
+  const int64_t n = int64_t(H) * W;
+  const int64_t m = airlight_count(H, W, fraction);
+  PDZ_REQUIRE(m >= 1 && m <= n, "airlight count %lld out of range", (long long)m);
+  select_init_kernel<<<batch, 256, 0, s>>>(L.st, (unsigned long long)m);
+  const int hist_gx = std::max(1, grid_for(n) / std::min(batch, 8));
+  for (int pass = 7; pass >= 0; --pass) {
+    select_hist_kernel<<<dim3(hist_gx, batch), 256, 0, s>>>(dark, n, L.st, pass * 8);
+    select_digit_kernel<<<batch, 256, 0, s>>>(L.st, pass * 8);
+  }
+  PDZ_CHECK_LAUNCH("radix select");
+  const int nb = int((n + kSelBlock - 1) / kSelBlock);
+  select_count_kernel<<<dim3(nb, batch), kSelThreads, 0, s>>>(dark, n, L.st, L.gt, L.eq);
+  select_scan_kernel<<<batch, 1024, 0, s>>>(L.gt, L.eq, nb);
+  select_compact_kernel<<<dim3(nb, batch), kSelThreads, 0, s>>>(
+      dark, n, L.st, L.gt, L.eq, (unsigned long long)m, L.ckey, L.cidx);
+  select_rank_kernel<<<dim3(int((m + 63) / 64), batch), 256, 0, s>>>(L.ckey, L.cidx, m, L.sorted);
+  const dim3 gg(grid_for(m), batch);
+  if (is_f64)
+    airlight_gather_kernel<double><<<gg, 256, 0, s>>>(image, C, L.sorted, m, L.vals, n);
+  else
+    airlight_gather_kernel<float><<<gg, 256, 0, s>>>(image, C, L.sorted, m, L.vals, n);
+  airlight_mean_kernel<<<dim3(C, batch), 256, 0, s>>>(L.vals, C, m, airlight);
+  PDZ_CHECK_LAUNCH("airlight");
+  return PDZ_OK;
+}
+
 int32_t pdz_atmospheric_light(const void* image, int32_t image_is_f64, int32_t height,
                               int32_t width, int32_t channels, const double* dark,
                               double fraction, double* airlight, int64_t* picked,
@@ -645,33 +732,113 @@ int32_t pdz_atmospheric_light(const void* image, int32_t image_is_f64, int32_t h
     return PDZ_EWORKSPACE;
   }
   cudaStream_t s = as_stream(stream);
-  const int64_t n = int64_t(height) * width;
-  const int64_t m = airlight_count(height, width, fraction);
-  PDZ_REQUIRE(m >= 1 && m <= n, "airlight count %lld out of range", (long long)m);
-  select_init_kernel<<<1, 256, 0, s>>>(L.st, (unsigned long long)m);
-  const int hist_grid = grid_for(n);
-  for (int pass = 7; pass >= 0; --pass) {
-    select_hist_kernel<<<hist_grid, 256, 0, s>>>(dark, n, L.st, pass * 8);
-    select_digit_kernel<<<1, 256, 0, s>>>(L.st, pass * 8);
-  }
-  PDZ_CHECK_LAUNCH("radix select");
-  const int nb = int((n + kSelBlock - 1) / kSelBlock);
-  select_count_kernel<<<nb, kSelThreads, 0, s>>>(dark, n, L.st, L.gt, L.eq);
-  select_scan_kernel<<<1, 1024, 0, s>>>(L.gt, L.eq, nb);
-  select_compact_kernel<<<nb, kSelThreads, 0, s>>>(dark, n, L.st, L.gt, L.eq,
-                                                   (unsigned long long)m, L.ckey, L.cidx);
-  select_rank_kernel<<<int((m + 63) / 64), 256, 0, s>>>(L.ckey, L.cidx, m, L.sorted);
-  if (image_is_f64)
-    airlight_gather_kernel<double><<<grid_for(m), 256, 0, s>>>(image, channels, L.sorted, m,
-                                                               L.vals);
-  else
-    airlight_gather_kernel<float><<<grid_for(m), 256, 0, s>>>(image, channels, L.sorted, m,
-                                                              L.vals);
-  airlight_mean_kernel<<<channels, 256, 0, s>>>(L.vals, channels, m, airlight);
-  PDZ_CHECK_LAUNCH("airlight");
+  const int32_t rc = airlight_impl(image, image_is_f64, height, width, channels, dark, fraction,
+                                   airlight, L, s, 1);
+  if (rc != PDZ_OK) return rc;
   if (picked)
-    PDZ_CUDA(cudaMemcpyAsync(picked, L.sorted, size_t(m) * 8, cudaMemcpyDeviceToDevice, s),
+    PDZ_CUDA(cudaMemcpyAsync(picked, L.sorted,
+                             size_t(airlight_count(height, width, fraction)) * 8,
+                             cudaMemcpyDeviceToDevice, s),
              "picked copy");
+  return PDZ_OK;
+}
+
+__global__ void fill_f64_kernel(double* p, int n, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// Workspace of the batched front end: three [batch][H][W] double planes
+// (dark + the two min-filter scratch planes), a [C] vector of ones, one more
+// plane for the multiscale blend, and the batched selection state.
+struct FrontLayout {
+  double *dark, *ta, *tb, *blend, *ones;
+  SelectLayout sel;
+  size_t bytes;
+};
+static FrontLayout carve_front(int B, int H, int W, int n_radii, double fraction, void* ws,
+                               size_t cap) {
+  Carver c(ws, cap);
+  FrontLayout F;
+  const size_t n = size_t(B) * H * W;
+  F.dark = c.take<double>(n);
+  F.ta = c.take<double>(n);
+  F.tb = c.take<double>(n);
+  F.blend = n_radii > 1 ? c.take<double>(n) : nullptr;
+  F.ones = c.take<double>(32);
+  const size_t head = Carver::round(c.off);
+  F.sel = carve_select(H, W, fraction, ws ? static_cast<char*>(ws) + head : nullptr,
+                       cap > head ? cap - head : 0, B);
+  F.bytes = head + Carver::round(F.sel.bytes);
+  return F;
+}
+
+size_t pdz_front_end_batch_workspace_bytes(int32_t batch, int32_t height, int32_t width,
+                                           int32_t n_radii, double fraction) {
+  if (batch < 1 || height < 1 || width < 1) return 0;
+  return carve_front(batch, height, width, n_radii, fraction, nullptr, 0).bytes;
+}
+
+int32_t pdz_front_end_batch(const void* images, int32_t image_is_f64, int32_t batch,
+                            int32_t height, int32_t width, int32_t channels,
+                            const int32_t* radii_host, const double* weights_host,
+                            int32_t n_radii, double fraction, double omega, double t_floor,
+                            int32_t lambda_mode, double lambda0, double beta, double* airlight,
+                            double* transmission, float* phi, float* lambda_map, double* phi64,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  PDZ_REQUIRE(images && radii_host && weights_host && airlight && transmission, "NULL argument");
+  PDZ_REQUIRE(batch >= 1 && batch <= 65535, "batch must lie in [1, 65535], got %d", batch);
+  PDZ_REQUIRE(height >= 1 && width >= 1 && channels >= 1 && channels <= 32, "bad image shape");
+  PDZ_REQUIRE(n_radii >= 1, "radii must be nonempty");
+  PDZ_REQUIRE(fraction > 0.0 && fraction <= 1.0, "fraction must lie in (0, 1]");
+  PDZ_REQUIRE(omega > 0.0 && omega <= 1.0, "omega must lie in (0, 1]");
+  PDZ_REQUIRE(t_floor > 0.0, "t_floor must be > 0");
+  PDZ_REQUIRE(lambda_mode >= 0 && lambda_mode <= 3, "bad lambda_mode %d", lambda_mode);
+  for (int k = 0; k < n_radii; ++k) PDZ_REQUIRE(radii_host[k] >= 0, "patch_radius must be >= 0");
+  FrontLayout F = carve_front(batch, height, width, n_radii, fraction, workspace, workspace_bytes);
+  if (workspace == nullptr || F.bytes > workspace_bytes) {
+    set_error("workspace too small: need %zu bytes, got %zu", F.bytes, workspace_bytes);
+    return PDZ_EWORKSPACE;
+  }
+  cudaStream_t s = as_stream(stream);
+  const int64_t n = int64_t(height) * width, nall = n * batch;
+  fill_f64_kernel<<<1, 32, 0, s>>>(F.ones, 32, 1.0);
+  // (multiscale_)dark_channel of every image for a per-image or shared A
+  auto dark_of = [&](const double* a, int a_stride) -> int32_t {
+    if (n_radii == 1 && weights_host[0] == 1.0)
+      return dark_channel_impl(images, image_is_f64, height, width, channels, a, radii_host[0],
+                               F.dark, F.ta, F.tb, s, batch, a_stride);
+    for (int k = 0; k < n_radii; ++k) {
+      const int32_t rc = dark_channel_impl(images, image_is_f64, height, width, channels, a,
+                                           radii_host[k], F.blend, F.ta, F.tb, s, batch,
+                                           a_stride);
+      if (rc != PDZ_OK) return rc;
+      blend_kernel<<<grid_for(nall), 256, 0, s>>>(F.blend, F.dark, nall, weights_host[k], k == 0);
+      PDZ_CHECK_LAUNCH("blend");
+    }
+    return PDZ_OK;
+  };
+  int32_t rc = dark_of(F.ones, 0);  // scattering.py:88-107 works on the A = 1 dark channel
+  if (rc != PDZ_OK) return rc;
+  rc = airlight_impl(images, image_is_f64, height, width, channels, F.dark, fraction, airlight,
+                     F.sel, s, batch);
+  if (rc != PDZ_OK) return rc;
+  rc = dark_of(airlight, channels);
+  if (rc != PDZ_OK) return rc;
+  transmission_kernel<<<grid_for(nall), 256, 0, s>>>(F.dark, nall, omega, transmission);
+  PDZ_CHECK_LAUNCH("transmission");
+  if (phi || lambda_map || phi64) {
+    const dim3 grid(std::max(1, grid_for(n) / std::min<int>(batch, 8)), batch);
+    if (image_is_f64)
+      fields_kernel<double><<<grid, 256, 0, s>>>(images, n, channels, transmission, airlight,
+                                                 t_floor, lambda_mode, lambda0, beta, phi,
+                                                 lambda_map, phi64);
+    else
+      fields_kernel<float><<<grid, 256, 0, s>>>(images, n, channels, transmission, airlight,
+                                                t_floor, lambda_mode, lambda0, beta, phi,
+                                                lambda_map, phi64);
+    PDZ_CHECK_LAUNCH("solver fields");
+  }
   return PDZ_OK;
 }
 

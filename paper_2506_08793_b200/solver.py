@@ -575,24 +575,60 @@ def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
     is_f64 = 1 if dtype == torch.float64 else 0
     phi = torch.empty((B * c, h, w), dtype=torch.float32, device=dev)
     lam = torch.empty((B, h, w), dtype=torch.float32, device=dev)
-    ts, airs, bounds = [], [], []
-    for i in range(B):
-        if i % 16 == 0:
-            main.wait_event(landed[i // 16])
-        t_dev, a_dev = _front_end(stack[i], is_f64, cfg, flags)
-        _, _, b = prepare_problem(stack[i], is_f64, t_dev, a_dev, cfg, _lambda_mode(flags, cfg),
-                                  phi=phi[i * c:(i + 1) * c], lam=lam[i], with_bounds=True)
-        ts.append(t_dev)
-        airs.append(a_dev)
-        bounds.append(b)
+    lib = nat.lib()
+    if "no-guided" in flags:
+        # every front-end stage is one launch sequence for the whole batch
+        # (pdz_front_end_batch; the guided refinement is per image)
+        main.wait_event(landed[-1])
+        if "no-multiscale" in flags:
+            radii, weights = (cfg.patch_radius,), (1.0,)
+        else:
+            radii, weights = _blend_weights(cfg.multiscale_radii, cfg.multiscale_weights)
+        if any(r < 0 for r in radii):
+            raise ValueError("patch_radius must be >= 0")
+        r_np = np.ascontiguousarray(radii, dtype=np.int32)
+        w_np = np.ascontiguousarray(weights, dtype=np.float64)
+        a_all = torch.empty((B, c), dtype=torch.float64, device=dev)
+        t_all = torch.empty((B, h, w), dtype=torch.float64, device=dev)
+        phi64 = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
+        ws = nat.workspace(lib.pdz_front_end_batch_workspace_bytes(
+            B, h, w, len(radii), float(cfg.airlight_fraction)), "front-batch")
+        nat.check(lib.pdz_front_end_batch(
+            nat.ptr(stack), is_f64, B, h, w, c, r_np.ctypes.data, w_np.ctypes.data, len(radii),
+            float(cfg.airlight_fraction), float(cfg.omega), float(cfg.t_floor),
+            int(_lambda_mode(flags, cfg)), float(cfg.lambda0), float(cfg.beta), nat.ptr(a_all),
+            nat.ptr(t_all), nat.ptr(phi), nat.ptr(lam), nat.ptr(phi64), nat.ptr(ws), ws.numel(),
+            nat.stream_ptr()))
+        # tau_stability_bound at u0 = Phi from the float64 Phi, image by image
+        prm = _params(h, w, c, c, cfg)
+        tws = nat.workspace(lib.pdz_tau_bound_workspace_bytes(prm), "tau")
+        bound_all = torch.empty((B, c), dtype=torch.float64, device=dev)
+        for i in range(B):
+            nat.check(lib.pdz_tau_bound_hwc(prm, nat.ptr(phi64[i]), nat.ptr(lam[i]),
+                                            nat.ptr(bound_all[i]), nat.ptr(tws), tws.numel(),
+                                            nat.stream_ptr()))
+        del phi64
+        bounds_cat = bound_all.reshape(-1)
+    else:
+        ts, airs, bounds = [], [], []
+        for i in range(B):
+            if i % 16 == 0:
+                main.wait_event(landed[i // 16])
+            t_dev, a_dev = _front_end(stack[i], is_f64, cfg, flags)
+            _, _, b = prepare_problem(stack[i], is_f64, t_dev, a_dev, cfg,
+                                      _lambda_mode(flags, cfg), phi=phi[i * c:(i + 1) * c],
+                                      lam=lam[i], with_bounds=True)
+            ts.append(t_dev)
+            airs.append(a_dev)
+            bounds.append(b)
+        t_all, a_all = torch.stack(ts), torch.stack(airs)
+        bounds_cat = torch.cat(bounds)
+        del ts, airs, bounds
     _, unit_check = validate_unit_image(stack.view(B * h, w, c), defer=True)
-    t_all, a_all = torch.stack(ts), torch.stack(airs)
-    del ts, airs
     t_host, a_host = to_host_async(t_all, like), to_host_async(a_all, like)
-    problem = DeviceProblem(phi, lam, h, w, B * c, c, torch.cat(bounds))
+    problem = DeviceProblem(phi, lam, h, w, B * c, c, bounds_cat)
     u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
-    lib = nat.lib()
     for i in range(B):
         nat.check(lib.pdz_clamp_interleave(nat.ptr(u[i * c:(i + 1) * c]), h, w, c,
                                            nat.ptr(out[i]), 1, nat.stream_ptr()))

@@ -317,19 +317,29 @@ def test_deterministic_bitwise(pdz):
         assert x.residual_norms == y.residual_norms
 
 
-def test_batch_equals_single(pdz):
+@pytest.mark.parametrize("flags,dtype", [
+    (("no-multiscale", "no-guided"), np.float64),   # batched front end, one radius
+    (("no-guided",), np.float32),                   # batched front end, multiscale blend
+    (("no-multiscale",), np.float64),               # guided refinement: per-image front ends
+])
+def test_batch_equals_single(pdz, flags, dtype):
+    """dehaze_batch against dehaze image by image: the airlight, the
+    transmission map, the restored image, the tau bounds and the traces are
+    bitwise equal (pdz_front_end_batch runs every stage once for the batch)."""
     from paper_2506_08793_b200.synthetic import make_hazy_scene
 
-    imgs = [make_hazy_scene(48, 80, 3, i).hazy.astype(np.float64) for i in range(5)]
-    cfg = pdz.SolverConfig(tau=TAU_STABLE, max_iters=25, rel_tol=1e-3)
-    out, res = pdz.dehaze_batch(imgs, cfg, ablation=("no-multiscale", "no-guided"))
+    imgs = [make_hazy_scene(48, 80, 3, i).hazy.astype(dtype) for i in range(5)]
+    cfg = pdz.SolverConfig(tau=TAU_STABLE, max_iters=25, rel_tol=1e-3, guided_radius=5)
+    out, res = pdz.dehaze_batch(imgs, cfg, ablation=flags)
     for i, im in enumerate(imgs):
-        o, r = pdz.dehaze(im, cfg, ablation=("no-multiscale", "no-guided"))
-        np.testing.assert_array_equal(out[i], o)
+        o, r = pdz.dehaze(im, cfg, ablation=flags)
         np.testing.assert_array_equal(res[i].airlight, r.airlight)
+        np.testing.assert_array_equal(res[i].transmission, r.transmission)
+        np.testing.assert_array_equal(out[i], o)
         for x, y in zip(res[i].traces, r.traces):
             assert x.residual_norms == y.residual_norms
             assert x.iterations_run == y.iterations_run
+            assert x.tau_bound == y.tau_bound
 
 
 # ---------------------------------------------------------------- edge cases
