@@ -459,6 +459,63 @@ def _front_end(img_dev, is_f64, cfg, flags):
     return t_dev, a_dev
 
 
+_stage_pinned = threading.local()
+
+
+def _pinned_like(array):
+    """A page-locked torch copy of a numpy array (one cached buffer per thread
+    and size; the upload that follows is asynchronous and runs at full rate)."""
+    import torch
+
+    buf = getattr(_stage_pinned, "buf", None)
+    nbytes = array.nbytes
+    if buf is None or buf.numel() < nbytes:
+        buf = _stage_pinned.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8,
+                                              pin_memory=True)
+    t = buf[:nbytes].view(torch.float32 if array.dtype == np.float32 else torch.float64)
+    t = t.view(array.shape)
+    t.copy_(torch.from_numpy(np.ascontiguousarray(array)))
+    return t
+
+
+def _front_end_fused(img_dev, is_f64, cfg, flags):
+    """(t, A, Phi, lambda, tau bounds) of one image without the guided
+    refinement: pdz_front_end_batch on a batch of one, then the float64 tau
+    bound.  Bitwise the values of _front_end + prepare_problem."""
+    import torch
+
+    h, w, c = img_dev.shape
+    lib = nat.lib()
+    if "no-multiscale" in flags:
+        radii, weights = (cfg.patch_radius,), (1.0,)
+    else:
+        radii, weights = _blend_weights(cfg.multiscale_radii, cfg.multiscale_weights)
+    if any(r < 0 for r in radii):
+        raise ValueError("patch_radius must be >= 0")
+    dev = img_dev.device
+    r_np = np.ascontiguousarray(radii, dtype=np.int32)
+    w_np = np.ascontiguousarray(weights, dtype=np.float64)
+    a_dev = torch.empty(c, dtype=torch.float64, device=dev)
+    t_dev = torch.empty((h, w), dtype=torch.float64, device=dev)
+    phi = torch.empty((c, h, w), dtype=torch.float32, device=dev)
+    lam = torch.empty((h, w), dtype=torch.float32, device=dev)
+    phi64 = torch.empty((h, w, c), dtype=torch.float64, device=dev)
+    ws = nat.workspace(lib.pdz_front_end_batch_workspace_bytes(
+        1, h, w, len(radii), float(cfg.airlight_fraction)), "front-batch")
+    nat.check(lib.pdz_front_end_batch(
+        nat.ptr(img_dev), is_f64, 1, h, w, c, r_np.ctypes.data, w_np.ctypes.data, len(radii),
+        float(cfg.airlight_fraction), float(cfg.omega), float(cfg.t_floor),
+        int(_lambda_mode(flags, cfg)), float(cfg.lambda0), float(cfg.beta), nat.ptr(a_dev),
+        nat.ptr(t_dev), nat.ptr(phi), nat.ptr(lam), nat.ptr(phi64), nat.ptr(ws), ws.numel(),
+        nat.stream_ptr()))
+    prm = _params(h, w, c, c, cfg)
+    tws = nat.workspace(lib.pdz_tau_bound_workspace_bytes(prm), "tau")
+    bounds = torch.empty(c, dtype=torch.float64, device=dev)
+    nat.check(lib.pdz_tau_bound_hwc(prm, nat.ptr(phi64), nat.ptr(lam), nat.ptr(bounds),
+                                    nat.ptr(tws), tws.numel(), nat.stream_ptr()))
+    return t_dev, a_dev, phi, lam, bounds
+
+
 def _image_dev(img):
     import torch
 
@@ -479,7 +536,16 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
     # deferred until the front end is queued, so the GPU never waits for the
     # host in between (the errors are the same and come before any result)
     dev_in = is_device_array(image)
-    img, unit_check = validate_unit_image(to_device(image) if dev_in else image, defer=dev_in)
+    staged = image
+    if (not dev_in and isinstance(image, np.ndarray) and image.ndim == 3
+            and image.dtype in (np.float32, np.float64)):
+        # numpy float images take the same road: staged through a page-locked
+        # buffer, uploaded as they are (float32 stays float32 -- its float64
+        # value is the same) and validated on the GPU, instead of a float64
+        # copy and three passes over it on the host
+        staged = _pinned_like(image)
+        dev_in = True
+    img, unit_check = validate_unit_image(to_device(staged) if dev_in else image, defer=dev_in)
     if workers < 1:
         if dev_in:
             unit_check()  # the finiteness error comes first, as in the reference
@@ -488,10 +554,25 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
         unit_check()
     img_dev, is_f64 = _image_dev(img)
     h, w, c = img_dev.shape
+    lib = nat.lib()
+    if "no-guided" in flags and "no-pde" not in flags and h >= 2 and w >= 2:
+        # no guided refinement: the whole front end and the solver inputs are
+        # one library call (pdz_front_end_batch with a batch of one)
+        t_dev, a_dev, phi, lam, bounds = _front_end_fused(img_dev, is_f64, cfg, flags)
+        if dev_in:
+            unit_check()
+        t_host, a_host = to_host_async(t_dev, image), to_host_async(a_dev, image)
+        u, finish = queue_solve_problem(DeviceProblem(phi, lam, h, w, c, c, bounds), cfg,
+                                        edge_preserving="no-edge" not in flags)
+        out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
+        nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1,
+                                           nat.stream_ptr()))
+        out_host = to_host_async(out, image)
+        traces = finish()
+        return (out_host(), DehazeResult(a_host(), t_host(), traces, flags))
     t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
     if dev_in:
         unit_check()
-    lib = nat.lib()
     if "no-pde" in flags:
         phi64 = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
         nat.check(lib.pdz_solver_fields(nat.ptr(img_dev), is_f64, h, w, c, nat.ptr(t_dev),
