@@ -168,6 +168,31 @@ PLAN_FIELDS = ("kind", "ctas", "ctas_per_strip", "bonus", "geometry", "radius",
                "channel_inner")
 
 
+class trace_range:
+    """NVTX range around a pipeline stage (front end, solve, result copies,
+    slab blocks, halo exchange) for nsys / ncu timelines; off unless PDZ_NVTX=1
+    (tracing)."""
+
+    enabled = os.environ.get("PDZ_NVTX", "") == "1"
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if self.enabled:
+            import torch
+
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if self.enabled:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
+        return False
+
+
 def plan_info(params) -> dict:
     """The launch plan of a solve (pdz_solve_plan_info; host only)."""
     buf = (ctypes.c_int32 * len(PLAN_FIELDS))()

@@ -346,8 +346,10 @@ class SlabSolver:
         while it < max_iters:
             k = min(self.k, max_iters - it)
             if it:  # u0 = Phi: every rank already holds its halo rows of it
-                self.exchange(eng.field())
-            sums, failed = eng.run(k, keep_start=False)
+                with nat.trace_range("pdz.slab.exchange"):
+                    self.exchange(eng.field())
+            with nat.trace_range("pdz.slab.block"):
+                sums, failed = eng.run(k, keep_start=False)
             table.append(sums)
             first = torch.where(failed > 0, failed + it, torch.zeros_like(failed))
             bad = first if bad is None else torch.where(bad > 0, bad, first)
@@ -388,8 +390,10 @@ class SlabSolver:
         while it < max_iters and any(running):
             k = min(self.k, max_iters - it)
             if it:
-                self.exchange(eng.field())
-            sums, failed = eng.run(k, keep_start=True)
+                with nat.trace_range("pdz.slab.exchange"):
+                    self.exchange(eng.field())
+            with nat.trace_range("pdz.slab.block"):
+                sums, failed = eng.run(k, keep_start=True)
             sums, failed = self._allreduce(sums, failed)
             sums_h = sums.to("cpu").numpy()
             failed_h = failed.to("cpu").numpy()

@@ -558,19 +558,22 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
     if "no-guided" in flags and "no-pde" not in flags and h >= 2 and w >= 2:
         # no guided refinement: the whole front end and the solver inputs are
         # one library call (pdz_front_end_batch with a batch of one)
-        t_dev, a_dev, phi, lam, bounds = _front_end_fused(img_dev, is_f64, cfg, flags)
+        with nat.trace_range("pdz.front_end"):
+            t_dev, a_dev, phi, lam, bounds = _front_end_fused(img_dev, is_f64, cfg, flags)
         if dev_in:
             unit_check()
         t_host, a_host = to_host_async(t_dev, image), to_host_async(a_dev, image)
-        u, finish = queue_solve_problem(DeviceProblem(phi, lam, h, w, c, c, bounds), cfg,
-                                        edge_preserving="no-edge" not in flags)
+        with nat.trace_range("pdz.solve"):
+            u, finish = queue_solve_problem(DeviceProblem(phi, lam, h, w, c, c, bounds), cfg,
+                                            edge_preserving="no-edge" not in flags)
         out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
         nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1,
                                            nat.stream_ptr()))
         out_host = to_host_async(out, image)
         traces = finish()
         return (out_host(), DehazeResult(a_host(), t_host(), traces, flags))
-    t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
+    with nat.trace_range("pdz.front_end"):
+        t_dev, a_dev = _front_end(img_dev, is_f64, cfg, flags)
     if dev_in:
         unit_check()
     if "no-pde" in flags:
@@ -591,7 +594,8 @@ def dehaze(image, cfg: SolverConfig | None = None, ablation=(), workers: int = 1
     problem = DeviceProblem(phi, lam, h, w, c, c, bounds)
     # clamp + interleave and the result copy are queued behind the solve
     # before the host reads the solve's outcome: the GPU never waits for it
-    u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    with nat.trace_range("pdz.solve"):
+        u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((h, w, c), dtype=torch.float64, device=img_dev.device)
     nat.check(lib.pdz_clamp_interleave(nat.ptr(u), h, w, c, nat.ptr(out), 1, nat.stream_ptr()))
     out_host = to_host_async(out, image)
@@ -708,7 +712,8 @@ def dehaze_batch(images, cfg: SolverConfig | None = None, ablation=()):
     _, unit_check = validate_unit_image(stack.view(B * h, w, c), defer=True)
     t_host, a_host = to_host_async(t_all, like), to_host_async(a_all, like)
     problem = DeviceProblem(phi, lam, h, w, B * c, c, bounds_cat)
-    u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
+    with nat.trace_range("pdz.solve_batch"):
+        u, finish = queue_solve_problem(problem, cfg, edge_preserving="no-edge" not in flags)
     out = torch.empty((B, h, w, c), dtype=torch.float64, device=dev)
     for i in range(B):
         nat.check(lib.pdz_clamp_interleave(nat.ptr(u[i * c:(i + 1) * c]), h, w, c,
