@@ -273,3 +273,27 @@ def test_channel_inner_block_order(pdz, monkeypatch, rel_tol):
             np.testing.assert_allclose(x.residual_norms, y.residual_norms, rtol=1e-8)
     monkeypatch.setenv("PDZ_STREAM_CI", "1")
     _check_against_oracle(runs["1"][0][3], runs["1"][1][3], imgs[3], cfg)
+
+
+def test_config3_full_batch_of_256(pdz):
+    """The whole config-3 batch (256 x 640x480x3) through dehaze_batch for a
+    few sweeps -- the batched front end, the channel-inner plan and one
+    persistent launch over 768 planes -- and, as its size-independent check,
+    images from the start, the middle and the end of the batch bitwise equal to
+    their single-image dehaze (which the other tests tie to the oracle)."""
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import _params
+
+    cfg = _cfg(pdz, 3, max_iters=4)
+    plan = nat.plan_info(_params(480, 640, 3 * 256, 3, cfg))
+    assert plan["kind"] == 2 and plan["channel_inner"] == 1, plan
+    imgs = [SYN.make_hazy_scene(480, 640, 3, i % 24).hazy for i in range(256)]  # float32
+    out, res = pdz.dehaze_batch(imgs, cfg, ablation=FLAGS)
+    assert out.shape == (256, 480, 640, 3) and len(res) == 256
+    assert np.isfinite(out).all()
+    for i in (0, 131, 255):
+        o, r = pdz.dehaze(imgs[i], cfg, ablation=FLAGS)
+        np.testing.assert_array_equal(out[i], o)
+        np.testing.assert_array_equal(res[i].airlight, r.airlight)
+        np.testing.assert_array_equal(res[i].transmission, r.transmission)
+        assert [t.iterations_run for t in res[i].traces] == [4, 4, 4]

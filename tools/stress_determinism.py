@@ -61,6 +61,29 @@ def main():
     cfg_bs = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=120, rel_tol=2e-3)
     extra.append(("dehaze_batch stop-rule 6x100x200",
                   lambda: _dzb(pdz.dehaze_batch(batch_s, cfg_bs, abl))))
+    # round 2: the channel-inner block order (forced: these batches are far
+    # below the planner's 24-blocks-per-pass threshold), fixed sweeps and a
+    # staggered stop; a tall K = 49 strip walk (H rows carried in the ring)
+    def forced_ci(fn):
+        def run():
+            os.environ["PDZ_STREAM_CI"] = "1"
+            try:
+                return fn()
+            finally:
+                del os.environ["PDZ_STREAM_CI"]
+        return run
+
+    batch_c = [make_hazy_scene(300, 256, 3, 30 + i).hazy.astype(np.float64) for i in range(8)]
+    cfg_c = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=6, rel_tol=1e-300)
+    cfg_cs = pdz.SolverConfig(tau=TAU, kernel_size=13, sigma=2.0, max_iters=90, rel_tol=3e-3)
+    extra.append(("channel-inner batch 8x300x256",
+                  forced_ci(lambda: _dzb(pdz.dehaze_batch(batch_c, cfg_c, abl)))))
+    extra.append(("channel-inner stop-rule batch 8x300x256",
+                  forced_ci(lambda: _dzb(pdz.dehaze_batch(batch_c, cfg_cs, abl)))))
+    tall = make_hazy_scene(1500, 128, 3, 40).hazy.astype(np.float64)
+    cfg_t = pdz.SolverConfig(tau=TAU, kernel_size=49, sigma=8.0, max_iters=4, rel_tol=1e-300)
+    extra.append(("dehaze 1500x128 K=49 (carried H rows)",
+                  lambda: _dz(pdz.dehaze(tall, cfg_t, abl))))
     first = {}
     bad = 0
     for rep in range(args.reps):
