@@ -621,3 +621,53 @@ def test_every_odd_kernel_size_takes_the_persistent_kernel(pdz, k):
     ru, rtr = orc.relaxed_solve(ch, t, 0.9, orc.SolverSettings.from_config(cfg), separable=True)
     assert np.max(np.abs(u - ru)) <= U_TOL
     np.testing.assert_allclose(tr.residual_norms, rtr.residual_norms, rtol=NORM_RTOL)
+
+
+def _random_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        k = int(rng.choice([1, 3, 5, 7, 9, 11, 13, 15, 19, 21, 25, 29, 33, 41, 49]))
+        r = max(1, k // 2)
+        h = int(rng.integers(max(2 * r + 2, 8), 420))
+        w = int(rng.integers(max(2 * r + 8, 8), 420))
+        if rng.random() < 0.6:
+            w -= w % 4  # the persistent kernel's widths; the rest exercise the tiled one
+        planes = int(rng.choice([1, 2, 3, 6]))
+        channels = planes if planes <= 3 else 3
+        iters = int(rng.integers(1, 9))
+        cases.append((h, w, k, planes, channels, iters, bool(rng.random() < 0.8)))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_cases(24, 20260817))
+def test_random_shapes_against_oracle(pdz, case):
+    """Seeded random (H, W, K, planes, sweeps, edge on/off): whatever plan the
+    library picks (persistent or tiled, either geometry, rounded-up radius,
+    partial strips, batches of planes sharing lambda), every plane matches
+    the oracle to 1e-4 and its norms to 1e-5."""
+    import torch
+
+    from paper_2506_08793_b200 import _native as nat
+    from paper_2506_08793_b200.solver import DeviceProblem, solve_problem
+
+    h, w, k, planes, channels, iters, edge = case
+    rng = np.random.default_rng(h * 1000 + w + k)
+    phi = rng.uniform(0.0, 1.0, (planes, h, w)).astype(np.float32)
+    lam = rng.uniform(0.05, 0.5, (planes // channels, h, w)).astype(np.float32)
+    cfg = pdz.SolverConfig(tau=TAU_STABLE if edge else 0.05, kernel_size=k,
+                           sigma=max(0.8, k / 6.0), max_iters=iters, rel_tol=1e-300)
+    dev = nat.device()
+    prob = DeviceProblem(torch.from_numpy(phi).to(dev), torch.from_numpy(lam).to(dev), h, w,
+                         planes, channels, np.ones(planes))
+    u, traces = solve_problem(prob, cfg, edge_preserving=edge, warn=False)
+    u = u.cpu().numpy()
+    st = orc.SolverSettings.from_config(cfg)
+    for p in range(planes):
+        src, lm = phi[p].astype(np.float64), lam[p // channels].astype(np.float64)
+        ru, norms = src, []
+        for _ in range(iters):
+            ru, nrm = orc.relaxed_step(ru, src, lm, st, edge_preserving=edge, separable=True)
+            norms.append(nrm)
+        assert np.max(np.abs(u[p] - ru)) <= U_TOL, (case, p)
+        np.testing.assert_allclose(traces[p].residual_norms, norms, rtol=NORM_RTOL)
